@@ -1,0 +1,135 @@
+"""Pins of the oracle's GMRES and CN time loop: textbook GMRES facts, the direct solution
+of Eq.(tls), the exact-preconditioner special case, the paper's Table 1 iteration counts
+and errors, Theorem 3.7's mesh independence, and the CN / compact-scheme orders."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import dense as D
+from oracle import scheme
+from oracle.gmres import gmres
+from paper_2404_10221_b200 import inputs as I
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ---------------------------------------------------------------- GMRES [Saad86]
+def test_gmres_identity_one_iteration():
+    c = np.random.default_rng(0).standard_normal(10)
+    r = gmres(lambda v: v, c, np.zeros(10), 5, 1e-12, 50)
+    assert r.iters == 1 and r.converged and np.allclose(r.x, c, atol=1e-15)
+
+
+def test_gmres_diagonal_exact_in_n_steps():
+    d = np.array([1.0, 2.0, 3.0, 4.0])
+    c = np.ones(4)
+    r = gmres(lambda v: d * v, c, np.zeros(4), 10, 1e-13, 50)
+    assert r.converged and r.iters <= 4 and np.allclose(r.x, c / d, atol=1e-12)
+
+
+def test_gmres_minimal_residual_property():
+    rng = np.random.default_rng(1)
+    A = np.eye(12) * 3 + rng.standard_normal((12, 12)) * 0.3
+    c = rng.standard_normal(12)
+    x0 = rng.standard_normal(12)
+    r0 = c - A @ x0
+    for k in (1, 3, 6):
+        res = gmres(lambda v: A @ v, c, x0, 20, 0.0, 100, fixed_iters=k)
+        # explicit Krylov basis K_k(A, r0) and dense least squares
+        Kb = np.stack([np.linalg.matrix_power(A, i) @ r0 for i in range(k)], axis=1)
+        y, *_ = np.linalg.lstsq(A @ Kb, r0, rcond=None)
+        best = np.linalg.norm(r0 - A @ Kb @ y)
+        assert abs(np.linalg.norm(c - A @ res.x) - best) < 1e-10 * np.linalg.norm(r0)
+
+
+def test_gmres_restart_and_cap():
+    rng = np.random.default_rng(2)
+    A = np.eye(30) + np.diag(np.linspace(0, 20, 30))
+    c = rng.standard_normal(30)
+    r = gmres(lambda v: A @ v, c, np.zeros(30), 4, 1e-10, 400)
+    assert r.converged and r.iters > 4
+    assert np.linalg.norm(A @ r.x - c) < 1e-9 * np.linalg.norm(c)
+    capped = gmres(lambda v: A @ v, c, np.zeros(30), 4, 1e-14, 6)
+    assert not capped.converged and capped.iters == 6
+
+
+# ---------------------------------------------------------------- CN step vs direct solve
+@pytest.mark.parametrize("shape", [(9,), (5, 4), (4, 3, 5)])
+def test_time_loop_equals_direct_solution(shape):
+    d = len(shape)
+    p = I.config_c5(M=3, nn=shape) if d == 3 else (I.config_c1(n=shape[0], M=3) if d == 1 else I.config_c2(n=5, M=3))
+    if d == 2:
+        p.n = shape
+        p.source = lambda xs, t: np.cos(xs[0] + 2 * xs[1] + t)
+    u, rep, ebar = scheme.solve(p, tol=1e-13, tier="D")
+    # direct: A^{(m)} u^{(m+1)} = b^{(m)} via dense LU (Eq.(tls))
+    Ds = D.DenseSystem(p.d, p.n, p.alpha, p.kappa, p.tau)
+    v = D.vec(p.psi_interior())
+    for m in range(p.M):
+        e = p.e_grid(p.t_half(m))
+        v = np.linalg.solve(Ds.A(e), Ds.b(e, v, D.vec(scheme.source_F(p, m))))
+    assert np.max(np.abs(D.vec(u) - v)) < 1e-10 * max(1e-30, np.abs(v).max())
+    # tier L runs the same Krylov process: same counts, same solution
+    uL, repL, _ = scheme.solve(p, tol=1e-13, tier="L")
+    assert repL.iters == rep.iters
+    assert np.max(np.abs(uL - u)) < 1e-12 * np.abs(u).max()
+
+
+@pytest.mark.parametrize("shape", [(31,), (9, 7), (5, 4, 6)])
+def test_exact_preconditioner_alpha_two(shape):
+    # alpha = 2 on every axis: s = [2,-1,0..] so H(S) = 0 and tau(S_alpha) = S_alpha; with constant
+    # e = ebar, P_hat = A exactly and one-sided GMRES converges in exactly one iteration.
+    d = len(shape)
+    p = I.config_c5(M=2, nn=(3, 3, 3))
+    p.d, p.n = d, shape
+    p.alpha, p.kappa = (2.0,) * d, (1.0, 0.5, 2.0)[:d]
+    p.coeff = I.SeparableCoeff(a=lambda t: 1.5, b=lambda t: 0.0, g=[None] * d, k=[None] * d)
+    p.source = lambda xs, t: np.zeros([x.size for x in xs]) + 1.0
+    p.psi = lambda xs: 0.0
+    u, rep, ebar = scheme.solve(p, tol=1e-12, tier="L")
+    assert ebar == 1.5 and rep.iters == [1, 1]
+
+
+# ---------------------------------------------------------------- paper Table 1
+def _table1_rows():
+    rows = []
+    with open(os.path.join(GOLD, "table1_it_u.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                M, N1, a, it, err, _src = line.split()
+                rows.append((int(M), int(N1), float(a), float(it), float(err)))
+    return rows
+
+
+@pytest.mark.parametrize("row", _table1_rows(), ids=lambda r: f"M{r[0]}-N{r[1]}-a{r[2]}")
+def test_table1_iterations_and_error(row):
+    M, N1, alpha, it_paper, err_paper = row
+    p = I.example(1, N1 - 1, M, (alpha,))
+    u, rep, _ = scheme.solve(p)
+    assert all(rep.converged)
+    assert abs(rep.mean_iters - it_paper) <= 1.0
+    err = np.linalg.norm(u - p.exact(p.mesh(), 1.0))          # Error := ||u* - u||_2
+    assert err_paper / 3 < err < err_paper * 3
+
+
+# ---------------------------------------------------------------- Theorem 3.7 / orders
+def test_mesh_independent_iterations():
+    # Theorem 3.7: the rate is independent of N -- counts flat as n doubles (C5 analogue)
+    means = []
+    for n in (7, 15, 31):
+        p = I.config_c5(M=4, nn=(n, n, n))
+        _, rep, _ = scheme.solve(p)
+        means.append(rep.mean_iters)
+    assert max(means) - min(means) <= 1.0, means
+
+
+def test_crank_nicolson_second_order_in_time():
+    errs = []
+    for M in (4, 8, 16):
+        p = I.example(1, 255, M, (1.5,))
+        u, _, _ = scheme.solve(p, tol=1e-13)
+        errs.append(np.abs(u - p.exact(p.mesh(), 1.0)).max())
+    r = [errs[0] / errs[1], errs[1] / errs[2]]
+    assert all(3.6 < x < 4.4 for x in r), r
