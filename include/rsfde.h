@@ -1,0 +1,178 @@
+/*
+ * rsfde.h -- C ABI of the B200 (sm_100a) tau-preconditioned GMRES solver for the
+ * Crank-Nicolson / quasi-compact discretisation of the d-dimensional Riesz space
+ * fractional diffusion equation of arXiv 2404.10221 (PAPER.md, cited as P:<line>).
+ *
+ *   e(x,t) d_t u = sum_i kappa_i d^{alpha_i} u + f  on (0,1)^d,  u = 0 on the boundary
+ *
+ * Per CN step m the library solves Eq.(tls)
+ *     A^{(m)} u^{(m+1)} = (H_alpha E^{(m+1/2)} + S_alpha) u^{(m+1)}
+ *                       = (H_alpha E^{(m+1/2)} - S_alpha) u^{(m)} + tau F^{(m+1/2)} = b^{(m)}
+ * with GMRES preconditioned on the left by the sine-transform (tau) preconditioner.  The
+ * paper's one-sided system P_alpha^{-1} A~ u = P_alpha^{-1} b~ (Eq.(one-sided), P:217-221,
+ * A~ = E + H^{-1} S_alpha, b~ = H^{-1} b) is the same Krylov process as
+ * P_hat^{-1} A u = P_hat^{-1} b with P_hat = H_alpha P_alpha = ebar H_alpha + tau(S_alpha),
+ * because tau matrices commute; the default "A form" runs the latter.
+ *
+ * Conventions
+ *  - All compute runs in hand-written FP64 CUDA kernels on the stream passed in (a
+ *    cudaStream_t given as void*; NULL = legacy default stream).  There is no CPU fallback:
+ *    without a usable CUDA device every call returns RSFDE_E_CUDA.
+ *  - Grid vectors are FP64 values at the interior nodes x_J = (j_1 h_1, ..., j_d h_d),
+ *    h_i = 1/(n_i+1), j_i = 1..n_i, stored densely in C order [x_1][x_2][x_3]
+ *    (x_d fastest), N = prod n_i values.  (The paper's vector orders x_1 fastest, P:104;
+ *    the values are the same grid function.)
+ *  - Unless stated otherwise vector arguments are caller-owned DEVICE pointers.  The ctx
+ *    owns its tables, Krylov basis and work buffers (padded private layout).
+ *  - A ctx is used by one host thread at a time.  Calls are stream-ordered; only GMRES
+ *    calls synchronise the stream (once per Arnoldi step, to read the convergence flag).
+ *  - Restriction: every n_i + 1 must be a power of two with 2 <= n_i + 1 <= 512 (FFT lengths
+ *    L = 2(n_i+1) <= 1024 are built); otherwise RSFDE_E_DIM.  The paper's grids (N+1 = 2^k,
+ *    P:532-633) and BASELINE configs C1, C2, C4, C5 satisfy it; C3 (n = 2047) does not yet.
+ */
+#ifndef RSFDE_H
+#define RSFDE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rsfde_ctx rsfde_ctx; /* opaque */
+
+typedef enum {
+  RSFDE_OK = 0,
+  RSFDE_E_DIM = 1,    /* d not in {1,2,3}, n_i < 1, n_i+1 not a power of two or too large, NULL vector */
+  RSFDE_E_DOMAIN = 2, /* alpha_i not in (1,2] (alpha = 2 kept as the classical limit), kappa_i <= 0,
+                         tau_t <= 0, M < 1, m out of [0, M) */
+  RSFDE_E_COEFF = 3,  /* e-check <= 0: e must be positive with a positive minimum */
+  RSFDE_E_CONFIG = 4, /* missing coefficient tables, bad GMRES configuration */
+  RSFDE_E_CUDA = 5,   /* CUDA error (message in rsfde_last_error) */
+  RSFDE_E_NCCL = 6,   /* reserved: multi-GPU slab sharding is not in this version */
+  RSFDE_E_NOMEM = 7   /* device allocation failed */
+} rsfde_status;
+
+/* coefficient e(x,t) at the half levels t_{m+1/2} = (m+1/2) tau (Eq.(tls)) */
+enum { RSFDE_COEF_SEPARABLE = 0, RSFDE_COEF_GRID = 1 };
+
+typedef struct {
+  int kind;
+  /* SEPARABLE: e(x, t_{m+1/2}) = a_half[m] + b_half[m] * prod_i g_i(x_i) + sum_i k_i(x_i)
+     (all five BASELINE configs and the paper's Examples 1-3 have this form).
+     Host arrays, copied at setup: a_half, b_half of length M; g[i], k[i] of length n_i
+     sampled at the interior nodes of axis i; NULL g[i] means 1, NULL k[i] means 0. */
+  const double *a_half, *b_half;
+  const double *g[3], *k[3];
+  /* GRID: device pointer to e at the interior nodes in the dense layout, M*N values
+     (step m at offset m*N) or N values if grid_static != 0.  Not copied: must stay valid. */
+  const double *grid;
+  int grid_static;
+} rsfde_coeff;
+
+typedef struct {
+  int d;             /* 1, 2 or 3 */
+  int n[3];          /* interior points per axis (n_i = N in the paper) */
+  double alpha[3];   /* fractional orders, 1 < alpha_i <= 2 */
+  double kappa[3];   /* diffusion coefficients > 0 */
+  double tau_t;      /* time step tau = T/M */
+  int M;             /* number of CN steps (defines the half levels for e-bar) */
+  rsfde_coeff e;
+} rsfde_problem;
+
+/* operators for rsfde_matvec (x -> y, time level m for E^{(m+1/2)}) */
+enum {
+  RSFDE_OP_A = 0,           /* A^{(m)} = H_alpha E + S_alpha                       (Eq.(tls)) */
+  RSFDE_OP_ATILDE = 1,      /* A~ = E + H_alpha^{-1} S_alpha                        (Eq.(equi)) */
+  RSFDE_OP_S_ALPHA = 2,     /* S_alpha, Eq.(Salpha)                                          */
+  RSFDE_OP_H_ALPHA = 3,     /* H_alpha = H_{alpha_d} (x) ... (x) H_{alpha_1}       */
+  RSFDE_OP_H_ALPHA_INV = 4, /* H_alpha^{-1} (H is a tau matrix)                                */
+  RSFDE_OP_K = 5            /* the preconditioned operator P_hat^{-1} A = P_alpha^{-1} A~     */
+};
+
+/* preconditioners for rsfde_precond_apply */
+enum {
+  RSFDE_PHAT_INV = 0,        /* (ebar H_alpha + tau(S_alpha))^{-1} = S Lambda_hat^{-1} S              */
+  RSFDE_PALPHA_INV = 1,      /* P_alpha^{-1} = S Lambda_P^{-1} S, P_alpha of Eq.(Pa)          */
+  RSFDE_PALPHA_INV_SQRT = 2  /* P_alpha^{-1/2} = S Lambda_P^{-1/2} S (Eq.(Pls))                */
+};
+
+enum { RSFDE_X0_PREV = 0, RSFDE_X0_ZERO = 1 };
+enum { RSFDE_FORM_A = 0, RSFDE_FORM_ATILDE = 1 };
+
+typedef struct {
+  int restart;      /* GMRES(m) restart length, 1..50 */
+  int max_iters;    /* cap on Arnoldi steps per solve (<= 0: 10*restart) */
+  double tol;       /* stop when |g_{j+1}| <= tol * ||r_0|| (preconditioned residual) */
+  int x0_policy;    /* RSFDE_X0_PREV: x_0 = u^{(m)} (default); RSFDE_X0_ZERO */
+  int form;         /* RSFDE_FORM_A (default) or RSFDE_FORM_ATILDE (literal A~ / P_alpha chain) */
+  int fixed_iters;  /* > 0: run exactly this many Arnoldi steps (replay mode for parity) */
+} rsfde_gmres_cfg;
+
+typedef struct {
+  int *iters;               /* caller arrays of length m_count, may be NULL */
+  double *final_relres;     /* |g_{k+1}| / ||r_0|| at the last step of each solve */
+  unsigned char *converged;
+  double loop_seconds;      /* device time of the step loop (CUDA events) */
+  double setup_seconds;     /* host time of rsfde_setup */
+  long long total_iters;
+} rsfde_report;
+
+/* Set up: validate, build the 1-D tables on the host in long double (FCD generator P:124-127
+   with the alpha/2+k reading, tau eigenvalues q_i (P:158 with divisor N+1), circulant
+   spectra, twiddles, lambda^H), upload them, reduce e-hat/e-check on the device
+   (P:188-194).  *out receives a new context or NULL on error. */
+rsfde_status rsfde_setup(rsfde_ctx **out, const rsfde_problem *p, void *stream);
+
+/* y = op x (device pointers, dense layout, must not alias). */
+rsfde_status rsfde_matvec(rsfde_ctx *ctx, int op, int m, const double *x, double *y, void *stream);
+
+/* y = P^{-1} x for the preconditioner kind (device pointers, dense layout, may not alias). */
+rsfde_status rsfde_precond_apply(rsfde_ctx *ctx, int kind, const double *x, double *y, void *stream);
+
+/* One GMRES solve of A^{(m)} x = b (device pointers, dense layout): x holds x_0 on entry and
+   the solution on exit.  iters/relres/converged are host outputs (may be NULL). */
+rsfde_status rsfde_gmres_step(rsfde_ctx *ctx, int m, const double *b, double *x, const rsfde_gmres_cfg *cfg,
+                              int *iters, double *relres, int *converged, void *stream);
+
+/* March m_count CN steps from level m_begin: u holds u^{(m_begin)} on entry and
+   u^{(m_begin+m_count)} on exit.  F holds F^{(m+1/2)} (the compact-stencil source of the
+   Appendix) per step (m_count*N values, step k at offset k*N) or one static
+   vector (F_static != 0); F == NULL means F = 0.  u and F may be DEVICE or HOST pointers
+   (host pointers are staged through device memory inside the call; the copies are timed
+   in loop_seconds).  Returns RSFDE_OK also when a step did not converge: the report flags
+   it and the march stops at that step (rep->iters of later steps = -1). */
+rsfde_status rsfde_solve_steps(rsfde_ctx *ctx, int m_begin, int m_count, double *u, const double *F, int F_static,
+                               const rsfde_gmres_cfg *cfg, rsfde_report *rep, void *stream);
+
+/* F^{(m+1/2)} from f(., t_{m+1/2}) sampled on the CLOSED grid (n_i + 2 points per axis, dense C
+   layout, boundary samples included): F = (prod_l calH_{alpha_l} f) restricted to the interior,
+   calH_l g_j = (1 - alpha_l/12) g_j + alpha_l/24 (g_{j-1} + g_{j+1}) (Eq.(2.2)).  This
+   equals the Appendix vectors for d = 1, 2 and is the reading of the garbled d = 3
+   Appendix.  Device pointers; N outputs. */
+rsfde_status rsfde_compact_source(rsfde_ctx *ctx, const double *f_closed, double *F, void *stream);
+
+/* e-bar = (e-hat + e-check)/2 (Eq.(bard)) and the extremes (host outputs). */
+rsfde_status rsfde_ebar(const rsfde_ctx *ctx, double *ebar, double *ehat, double *echeck);
+
+/* Copy a 1-D setup table of axis i (0-based) to host memory `out` (n_i values unless
+   stated): which = 0 FCD generator s_k (k=0..n-1), 1 tau eigenvalues q, 2 lambda^H,
+   3 circulant spectrum c^ (L = 2(n_i+1) values, NOT divided by L), 4 eta_i (1 value). */
+rsfde_status rsfde_table(const rsfde_ctx *ctx, int axis, int which, double *out);
+
+/* Bytes of device memory the context holds (tables, work vectors, basis). */
+long long rsfde_device_bytes(const rsfde_ctx *ctx);
+
+/* Kernel launches issued since setup (or the last reset) -- evidence for bench.py. */
+long long rsfde_launch_count(const rsfde_ctx *ctx, int reset);
+
+/* Last error message of ctx (or of the last failed setup if ctx == NULL). */
+const char *rsfde_last_error(const rsfde_ctx *ctx);
+
+void rsfde_destroy(rsfde_ctx *ctx);
+
+/* library version string */
+const char *rsfde_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSFDE_H */

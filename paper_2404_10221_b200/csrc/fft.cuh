@@ -1,0 +1,161 @@
+// FP64 FFT building blocks for sm_100a: in-register radix-2 DFTs and a two-stage
+// warp-group FFT of length L = E*G (E complex values per thread, G threads per
+// transform, G | 32, G <= E) with exactly one shared-memory exchange.
+//
+// Layouts of one length-L transform held by a group of G threads (thread g):
+//   column layout : v[m]          = x[g + G*m],            m  = 0..E-1
+//   row layout    : v[ri*G + k2]  = X[(g*R + ri) + E*k2],  ri = 0..R-1, k2 = 0..G-1, R = E/G
+// fft_fwd maps column -> row layout (X_k = sum_j x_j W_L^{jk}, W_L = exp(-2 pi i/L));
+// fft_inv maps row -> column layout (x_j = sum_k X_k W_L^{-jk}, unnormalised).
+//
+// Derivation (four-step / Cooley-Tukey with L = E*G): j = g + G m, k = k1 + E k2,
+//   X_{k1+E k2} = sum_g W_G^{g k2} [ W_L^{g k1} sum_m x_{g+G m} W_E^{m k1} ].
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dft_consts.cuh"
+
+namespace rsfde {
+
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 c_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 c_scale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 c_conj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 c_mul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 c_mulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+
+// v * W_n^e with W_n = exp(-2 pi i / n), n | 64, e and n compile-time after unrolling
+__device__ __forceinline__ double2 c_twc(double2 v, int e, int n) {
+  e &= (n - 1);
+  if (e == 0) return v;
+  if (4 * e == n) return make_double2(v.y, -v.x);          // * (-i)
+  if (2 * e == n) return make_double2(-v.x, -v.y);         // * (-1)
+  if (4 * e == 3 * n) return make_double2(-v.y, v.x);      // * (+i)
+  const int k = e * (64 / n);
+  const double c = dftc::C64(k);
+  const double s = -dftc::S64(k);
+  return make_double2(fma(v.x, c, -v.y * s), fma(v.x, s, v.y * c));
+}
+
+__host__ __device__ __forceinline__ constexpr int ilog2c(int n) {
+  int r = 0;
+  while ((1 << r) < n) ++r;
+  return r;
+}
+__host__ __device__ __forceinline__ constexpr int brevc(int i, int bits) {
+  int r = 0;
+  for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+  return r;
+}
+
+// In-register forward DFT of N points a[0], a[S], ..., a[(N-1)S]; natural order in and out.
+// Radix-2 decimation in frequency followed by the (free) bit-reversal renaming.
+template <int N, int S = 1>
+__device__ __forceinline__ void dft(double2* a) {
+  if (N == 1) return;
+#pragma unroll
+  for (int h = N / 2; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int i0 = 0; i0 < N; i0 += 2 * h) {
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const double2 u = a[(i0 + k) * S];
+        const double2 w = a[(i0 + k + h) * S];
+        a[(i0 + k) * S] = c_add(u, w);
+        a[(i0 + k + h) * S] = c_twc(c_sub(u, w), k, 2 * h);
+      }
+    }
+  }
+  constexpr int BITS = ilog2c(N);
+  double2 t[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) t[i] = a[i * S];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i * S] = t[brevc(i, BITS)];
+}
+
+// inverse (unnormalised) in-register DFT: conj(DFT(conj(a)))
+template <int N, int S = 1>
+__device__ __forceinline__ void idft(double2* a) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i * S].y = -a[i * S].y;
+  dft<N, S>(a);
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i * S].y = -a[i * S].y;
+}
+
+// v[k1] *= W_L^{+-g k1}, k1 = 0..E-1.  tw[k] = W_L^k (exact, host long double).
+// Powers W_L^{g b}, b < 8, by recurrence from the exact W_L^g; W_L^{8 a g} loaded exactly.
+template <int E, bool INV>
+__device__ __forceinline__ void twiddle_col(double2 (&v)[E], const double2* __restrict__ tw, int g, int L) {
+  const double2 w1 = __ldg(tw + g);
+  double2 wb[8];
+  wb[0] = make_double2(1.0, 0.0);
+  wb[1] = w1;
+#pragma unroll
+  for (int b = 2; b < 8; ++b) wb[b] = c_mul(wb[b - 1], w1);
+#pragma unroll
+  for (int a = 0; a < (E + 7) / 8; ++a) {
+    const double2 wa = (a == 0) ? make_double2(1.0, 0.0) : __ldg(tw + ((8 * a * g) & (L - 1)));
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int k1 = 8 * a + b;
+      if (k1 == 0 || k1 >= E) continue;
+      const double2 w = (a == 0) ? wb[b] : (b == 0 ? wa : c_mul(wa, wb[b]));
+      v[k1] = INV ? c_mulc(v[k1], w) : c_mul(v[k1], w);
+    }
+  }
+}
+
+// XOR swizzle of the exchange buffer (row k1, column t) -> conflict-free 16-byte accesses
+template <int E, int G>
+__device__ __forceinline__ int xidx(int k1, int t) {
+  constexpr int R = E / G;
+  return (G >= 8) ? (k1 * G + (t ^ ((k1 / R) & 7))) : (k1 * G + t);
+}
+
+// Forward FFT, column layout in -> row layout out.  buf: L double2 of shared memory owned
+// by this group.  Caller guarantees nobody else is reading buf (a __syncwarp precedes).
+template <int E, int G>
+__device__ __forceinline__ void fft_fwd(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw) {
+  constexpr int R = E / G;
+  constexpr int L = E * G;
+  dft<E>(v);
+  twiddle_col<E, false>(v, tw, g, L);
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < E; ++k1) buf[xidx<E, G>(k1, g)] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int ri = 0; ri < R; ++ri)
+#pragma unroll
+    for (int t = 0; t < G; ++t) v[ri * G + t] = buf[xidx<E, G>(g * R + ri, t)];
+#pragma unroll
+  for (int ri = 0; ri < R; ++ri) dft<G>(v + ri * G);
+}
+
+// Inverse (unnormalised) FFT, row layout in -> column layout out.
+template <int E, int G>
+__device__ __forceinline__ void fft_inv(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw) {
+  constexpr int R = E / G;
+  constexpr int L = E * G;
+#pragma unroll
+  for (int ri = 0; ri < R; ++ri) idft<G>(v + ri * G);
+  __syncwarp();
+#pragma unroll
+  for (int ri = 0; ri < R; ++ri)
+#pragma unroll
+    for (int t = 0; t < G; ++t) buf[xidx<E, G>(g * R + ri, t)] = v[ri * G + t];
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < E; ++k1) v[k1] = buf[xidx<E, G>(k1, g)];
+  twiddle_col<E, true>(v, tw, g, L);
+  idft<E>(v);
+}
+
+}  // namespace rsfde

@@ -1,0 +1,132 @@
+// Kernel parameter blocks and launch entry points shared by the library's .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rsfde {
+
+// Grid geometry of the internal layout: C order [x1][x2][x3] (x_d fastest), the last
+// dimension padded to P = n_d + 1 with a zero pad element (private layout).
+struct Geom {
+  int d;
+  int n[3];      // interior sizes (unused axes = 1)
+  int P;         // padded last dimension
+  long long NP;  // total padded length = prod_{i<d-1} n_i * P
+};
+
+// e(x, t_{m+1/2}) evaluated on the fly
+struct ECoef {
+  int kind;                  // 0: none (X = 0), 1: separable, 2: dense device grid
+  double a, b;               // a(t_{m+1/2}), b(t_{m+1/2})
+  const double* g[3];        // device, length n_i, or null (= 1)
+  const double* k[3];        // device, length n_i, or null (= 0)
+  const double* grid;        // kind 2: dense layout [x1][x2][x3], N values
+};
+
+enum SpecKind { SPEC_PHAT = 0, SPEC_PALPHA = 1, SPEC_PALPHA_SQRT = 2, SPEC_HINV = 3 };
+
+// spectrum tables for the preconditioner scaling on the last axis
+struct Spec {
+  int kind;
+  double ebar;
+  double eta[3];
+  const double* q[3];     // tau eigenvalues q_i(k), k = 1..n_i (device)
+  const double* lamH[3];  // H eigenvalues (device)
+};
+
+// first-axis source of the "X" channel of an operator pass
+enum XMode { X_INPUT = 0, X_E_TIMES_R = 1, X_ZERO = 2 };
+
+struct PassParams {
+  Geom geo;
+  int axis;              // 0-based
+  int n, N, L;           // axis length, N = n+1, L = 2N
+  long long stride;      // element stride along the axis
+  long long inner;       // strided axes: pencils per outer index (= stride)
+  long long npairs;      // number of pencil pairs
+  int contiguous;        // axis == d-1
+  // vectors
+  const double* X;
+  const double* R;
+  const double* B;       // additive vector (physical last pass)
+  double* Y;
+  double* C;
+  const double* rscale;  // device scalar multiplying R (lazy basis normalisation) or null
+  int xmode;
+  // coefficients
+  double hc0, hc1;       // H stencil: 1 - alpha/12, alpha/24
+  double eta;            // T coefficient (eta_i times sign / factor)
+  double ycoef, bcoef;   // physical last pass: Y = ycoef*y + bcoef*B
+  double dst_scale;      // sqrt(2/N)
+  ECoef e;
+  Spec spec;
+  // per-axis tables (device)
+  const double* chat;    // circulant spectrum / L, length L
+  const double2* tw;     // W_L^k, length L
+  const double* lamH;    // H eigenvalues of this axis (length n)
+};
+
+// host-side launchers (pass_kernels.cu)
+cudaError_t launch_oper_pass(const PassParams& p, bool spectral, bool last, cudaStream_t s);
+cudaError_t launch_dst_pass(const PassParams& p, bool last, cudaStream_t s);
+
+// krylov_kernels.cu
+struct KrylovDims {
+  long long NP;
+  int nblk;  // blocks used by the streaming reductions
+};
+cudaError_t launch_pack(const double* dense, double* padded, const Geom& g, cudaStream_t s);
+cudaError_t launch_unpack(const double* padded, double* dense, const Geom& g, cudaStream_t s);
+// partial[b*J + i] = sum over block b's elements of (s_i V_i) . z
+cudaError_t launch_dots(const double* const* V, const double* vscale, int J, const double* z,
+                        double* partial, long long NP, int nblk, cudaStream_t s);
+// partial[b*J+i] = sum (s_i V_i) . (z - sum_l c_l s_l V_l), c read from device array coef
+cudaError_t launch_dots_after_update(const double* const* V, const double* vscale, int J, const double* z,
+                                     const double* coef, double* partial, long long NP, int nblk,
+                                     cudaStream_t s);
+// out = z - sum_l (c1_l + c2_l) s_l V_l ; partial[b] = ||out||^2 over block b
+cudaError_t launch_update_norm(const double* const* V, const double* vscale, int J, const double* z,
+                               const double* c1, const double* c2, double* out, double* partial,
+                               long long NP, int nblk, cudaStream_t s);
+// x += sum_l y_l s_l V_l
+cudaError_t launch_axpy_basis(const double* const* V, const double* vscale, int J, const double* y,
+                              double* x, long long NP, cudaStream_t s);
+// out[i] = sum_b partial[b*J + i] (fixed order), one small block
+cudaError_t launch_reduce(const double* partial, int nblk, int J, double* out, cudaStream_t s);
+// norm of a vector: partial sums of squares
+cudaError_t launch_sumsq(const double* z, double* partial, long long NP, int nblk, cudaStream_t s);
+// y = a*x + b*y
+cudaError_t launch_axpby(double a, const double* x, double b, double* y, long long NP, cudaStream_t s);
+// F = prod_l calH_l f on the closed grid (dense layouts)
+cudaError_t launch_compact_source(const double* f_closed, double* F, const Geom& g, const double* alpha,
+                                  cudaStream_t s);
+// e-hat / e-check reduction over interior grid x M half levels
+cudaError_t launch_emaxmin(const ECoef& e, const double* a_half, const double* b_half, int M, int grid_static,
+                           const Geom& geo, double* partial, int nblk, cudaStream_t s);
+
+// GMRES control state on the device (one solve)
+struct GmresState {
+  // small fields first: the host reads back the first 24 bytes after every iteration
+  int converged;
+  int breakdown;
+  double relres;
+  double beta0;
+  double H[52 * 51];    // rotated Hessenberg R, column-major (ld = 52)
+  double cs[51], sn[51];
+  double g[52];
+  double y[51];
+  double hsum[52];      // h1 + h2 of the current column
+};
+// number of blocks (= partial sums) every streaming reduction uses for a vector of length NP
+int reduction_blocks(long long NP, int nblk);
+// reduce the norm partials, fill Hessenberg column j with h1 + h2, rotate, test convergence.
+cudaError_t launch_arnoldi_finish(GmresState* st, const double* h1, const double* h2,
+                                  const double* partial_nrm, int nblk, int j, double tol,
+                                  double* vscale_next, cudaStream_t s);
+// beta = ||r0||: st->g = [beta,0..], beta0, vscale[0] = 1/beta
+cudaError_t launch_gmres_init(GmresState* st, const double* partial_nrm, int nblk, double* vscale0,
+                              int first_cycle, cudaStream_t s);
+// y = R^{-1} g for k columns
+cudaError_t launch_gmres_solve_y(GmresState* st, int k, cudaStream_t s);
+
+}  // namespace rsfde

@@ -1,0 +1,5 @@
+// instantiation of the pencil-pass kernels for FFT length L = 64
+#include "pass_kernels.cuh"
+namespace rsfde {
+RSFDE_INSTANTIATE_L(32, 2)
+}

@@ -1,0 +1,808 @@
+// Host side of the rsfde C ABI (include/rsfde.h): setup tables, operator chains built from
+// the per-axis pencil passes, the GMRES driver and the CN time march.  Every step of the
+// numerical path runs in the kernels of pass_kernels.cu / krylov_kernels.cu; this file only
+// sequences launches and keeps device memory.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstddef>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rsfde.h"
+#include "kernels.cuh"
+
+using namespace rsfde;
+
+namespace {
+thread_local std::string g_setup_error;
+constexpr int kNblk = 148 * 8;
+}  // namespace
+
+struct rsfde_ctx {
+  int d = 0;
+  int n[3] = {1, 1, 1};
+  double alpha[3] = {2, 2, 2}, kappa[3] = {0, 0, 0};
+  double tau = 0;
+  int M = 0;
+  Geom geo{};
+  double eta[3] = {0, 0, 0};
+  // host copies of the 1-D tables (long double computed, FP64 stored)
+  std::vector<double> s_tab[3], q_tab[3], lamH_tab[3], chat_tab[3];
+  // device tables
+  double* d_chat[3] = {nullptr, nullptr, nullptr};
+  double2* d_tw[3] = {nullptr, nullptr, nullptr};
+  double* d_lamH[3] = {nullptr, nullptr, nullptr};
+  double* d_q[3] = {nullptr, nullptr, nullptr};
+  // coefficient e
+  int ekind = RSFDE_COEF_SEPARABLE;
+  std::vector<double> a_half, b_half;
+  double* d_g[3] = {nullptr, nullptr, nullptr};
+  double* d_k[3] = {nullptr, nullptr, nullptr};
+  double *d_ahalf = nullptr, *d_bhalf = nullptr;
+  const double* grid = nullptr;
+  int grid_static = 0;
+  double ebar = 0, ehat = 0, echeck = 0;
+  // work vectors (padded layout, zero pads)
+  double* W[4] = {nullptr, nullptr, nullptr, nullptr};
+  double *Z = nullptr, *X = nullptr, *BUF = nullptr, *U0 = nullptr, *FP = nullptr, *FH = nullptr;
+  double *TMP = nullptr, *TMP2 = nullptr;
+  std::vector<double*> V;
+  double* d_vscale = nullptr;
+  double *d_h1 = nullptr, *d_h2 = nullptr, *d_part = nullptr, *d_nrm = nullptr;
+  GmresState* d_state = nullptr;
+  void* h_flags = nullptr;  // pinned 16 bytes: converged, breakdown, relres
+  long long bytes = 0;
+  long long launches = 0;
+  double setup_seconds = 0;
+  std::string err;
+  std::vector<void*> allocs;
+};
+
+// ------------------------------------------------------------------------------ helpers
+static rsfde_status cuda_fail(rsfde_ctx* c, cudaError_t e, const char* what) {
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+  if (c) c->err = buf; else g_setup_error = buf;
+  return e == cudaErrorMemoryAllocation ? RSFDE_E_NOMEM : RSFDE_E_CUDA;
+}
+#define CK(expr, what)                                   \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, what); \
+  } while (0)
+#define CKL(expr, what)                                  \
+  do {                                                   \
+    c->launches++;                                       \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, what); \
+  } while (0)
+#define TRY(expr)                       \
+  do {                                  \
+    rsfde_status _s = (expr);           \
+    if (_s != RSFDE_OK) return _s;      \
+  } while (0)
+
+static rsfde_status dalloc(rsfde_ctx* c, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc");
+  c->allocs.push_back(*p);
+  c->bytes += (long long)bytes;
+  e = cudaMemset(*p, 0, bytes);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset");
+  return RSFDE_OK;
+}
+
+template <class T>
+static rsfde_status upload(rsfde_ctx* c, T** dst, const T* src, size_t count) {
+  TRY(dalloc(c, (void**)dst, count * sizeof(T)));
+  cudaError_t e = cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(c, e, "upload");
+  return RSFDE_OK;
+}
+
+static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------------------ setup tables
+// FCD generator: s_0 = Gamma(a+1)/Gamma(a/2+1)^2, s_k = (1 - (a+1)/(a/2+k)) s_{k-1}
+static void fcd_generator(double a, int n, std::vector<long double>& s) {
+  s.assign(n, 0.0L);
+  const long double al = a;
+  s[0] = tgammal(al + 1.0L) / (tgammal(al / 2.0L + 1.0L) * tgammal(al / 2.0L + 1.0L));
+  for (int k = 1; k < n; ++k) s[k] = (1.0L - (al + 1.0L) / (al / 2.0L + (long double)k)) * s[k - 1];
+}
+
+// sum_{j=0}^{n-1} w_j s_j cos(pi j k / N), w_0 = 1, w_j = 2: the tau eigenvalue q at index k
+// (k = 1..n, Eq.(q) P:158 with divisor N = n+1) and the circulant spectrum c^_k of the order
+// L = 2N embedding (c = [s_0..s_{n-1}, 0, 0, 0, s_{n-1}..s_1]) for k = 0..N.
+static long double cos_sum(const std::vector<long double>& s, int N, int k) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  long double acc = s[0];
+  const int n = (int)s.size();
+  for (int j = 1; j < n; ++j) {
+    const long long r = ((long long)j * k) % (2LL * N);
+    acc += 2.0L * s[j] * cosl(pi * (long double)r / (long double)N);
+  }
+  return acc;
+}
+
+static rsfde_status build_axis_tables(rsfde_ctx* c, int i) {
+  const int n = c->n[i], N = n + 1, L = 2 * N;
+  const long double pi = 3.141592653589793238462643383279502884L;
+  std::vector<long double> s;
+  fcd_generator(c->alpha[i], n, s);
+  c->s_tab[i].resize(n);
+  for (int k = 0; k < n; ++k) c->s_tab[i][k] = (double)s[k];
+  // circulant spectrum for k = 0..N (real, even: c^_{L-k} = c^_k); q_k = c^_k for k = 1..n
+  std::vector<double> chat(L), chatL(L);
+  c->chat_tab[i].resize(L);
+  c->q_tab[i].resize(n);
+  for (int k = 0; k <= N; ++k) {
+    const long double v = cos_sum(s, N, k);
+    c->chat_tab[i][k] = (double)v;
+    chatL[k] = (double)(v / (long double)L);
+    if (k > 0 && k < N) {
+      c->chat_tab[i][L - k] = (double)v;
+      chatL[L - k] = (double)(v / (long double)L);
+    }
+    if (k >= 1 && k <= n) c->q_tab[i][k - 1] = (double)v;
+  }
+  // lambda_k(H_alpha) = 1 - (alpha/6) sin^2(k pi/(2N))
+  c->lamH_tab[i].resize(n);
+  for (int k = 1; k <= n; ++k) {
+    const long double sn = sinl((long double)k * pi / (2.0L * N));
+    c->lamH_tab[i][k - 1] = (double)(1.0L - (long double)c->alpha[i] / 6.0L * sn * sn);
+  }
+  // twiddles W_L^k = exp(-2 pi i k / L)
+  std::vector<double2> tw(L);
+  for (int k = 0; k < L; ++k) {
+    const long double ang = 2.0L * pi * (long double)k / (long double)L;
+    tw[k] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+  }
+  // eta_i = kappa_i tau / (2 h_i^alpha_i), h_i = 1/(n_i+1)
+  const long double h = 1.0L / (long double)N;
+  c->eta[i] = (double)((long double)c->kappa[i] * (long double)c->tau / (2.0L * powl(h, (long double)c->alpha[i])));
+  TRY(upload(c, &c->d_chat[i], chatL.data(), L));
+  TRY(upload(c, &c->d_tw[i], tw.data(), L));
+  TRY(upload(c, &c->d_lamH[i], c->lamH_tab[i].data(), n));
+  TRY(upload(c, &c->d_q[i], c->q_tab[i].data(), n));
+  return RSFDE_OK;
+}
+
+// ------------------------------------------------------------------------------ passes
+static PassParams axis_params(const rsfde_ctx* c, int axis) {
+  PassParams p;
+  memset(&p, 0, sizeof p);
+  p.geo = c->geo;
+  p.axis = axis;
+  p.n = c->n[axis];
+  p.N = p.n + 1;
+  p.L = 2 * p.N;
+  p.contiguous = axis == c->d - 1;
+  long long stride = 1;
+  if (!p.contiguous) {
+    stride = c->geo.P;
+    for (int i = axis + 1; i < c->d - 1; ++i) stride *= c->n[i];
+  }
+  p.stride = stride;
+  p.inner = stride;
+  if (p.contiguous) {
+    const long long rows = c->geo.NP / c->geo.P;
+    p.npairs = (rows + 1) / 2;
+  } else {
+    p.npairs = c->geo.NP / p.n / 2;
+  }
+  p.hc0 = 1.0 - c->alpha[axis] / 12.0;
+  p.hc1 = c->alpha[axis] / 24.0;
+  p.dst_scale = std::sqrt(2.0 / (double)p.N);
+  p.ycoef = 1.0;
+  p.chat = c->d_chat[axis];
+  p.tw = c->d_tw[axis];
+  p.lamH = c->d_lamH[axis];
+  p.spec.ebar = c->ebar;
+  for (int i = 0; i < 3; ++i) {
+    p.spec.eta[i] = c->eta[i];
+    p.spec.q[i] = c->d_q[i];
+    p.spec.lamH[i] = c->d_lamH[i];
+  }
+  return p;
+}
+
+static ECoef ecoef_at(const rsfde_ctx* c, int m) {
+  ECoef e;
+  memset(&e, 0, sizeof e);
+  if (c->ekind == RSFDE_COEF_GRID) {
+    e.kind = 2;
+    e.grid = c->grid + (c->grid_static ? 0 : (long long)m * c->n[0] * c->n[1] * c->n[2]);
+  } else {
+    e.kind = 1;
+    e.a = c->a_half[m];
+    e.b = c->b_half[m];
+    for (int i = 0; i < 3; ++i) {
+      e.g[i] = c->d_g[i];
+      e.k[i] = c->d_k[i];
+    }
+  }
+  return e;
+}
+
+struct ChainArgs {
+  int xmode = X_E_TIMES_R;
+  const double* Xin = nullptr;  // X_INPUT source (first pass)
+  const double* R = nullptr;
+  const double* rscale = nullptr;
+  double etafac = 1.0;
+  bool spectral = false;
+  int spec = SPEC_PHAT;
+  double ycoef = 1.0;           // physical last pass: out = ycoef*y + bcoef*B
+  const double* B = nullptr;
+  double bcoef = 0.0;
+  int m = 0;
+};
+
+// chain of operator passes over the axes (see pass_kernels.cu header); out must not alias inputs
+static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cudaStream_t s) {
+  const int d = c->d;
+  const double* Xcur = a.Xin;
+  const double* Rcur = a.R;
+  int buf = 0;
+  for (int ax = 0; ax < d; ++ax) {
+    const bool last = ax == d - 1;
+    PassParams p = axis_params(c, ax);
+    p.xmode = ax == 0 ? a.xmode : X_INPUT;
+    p.X = Xcur;
+    p.R = Rcur;
+    p.rscale = ax == 0 ? a.rscale : nullptr;
+    p.eta = a.etafac * c->eta[ax];
+    if (ax == 0 && a.xmode == X_E_TIMES_R) p.e = ecoef_at(c, a.m);
+    p.spec.kind = a.spec;
+    if (last) {
+      p.Y = (a.spectral && d > 1) ? c->W[buf] : out;
+      p.ycoef = a.ycoef;
+      p.B = a.B;
+      p.bcoef = a.bcoef;
+    } else {
+      p.Y = c->W[buf];
+      p.C = c->W[buf + 1];
+    }
+    CKL(launch_oper_pass(p, a.spectral, last, s), "oper pass");
+    if (!last) {
+      Xcur = c->W[buf];
+      Rcur = c->W[buf + 1];
+      buf = (buf + 2) % 4;
+    }
+  }
+  if (a.spectral && d > 1) {
+    // inverse DSTs along axes d-2 .. 0
+    const double* in = c->W[buf];
+    for (int ax = d - 2; ax >= 0; --ax) {
+      PassParams p = axis_params(c, ax);
+      p.X = in;
+      double* o = ax == 0 ? out : c->W[(buf + 1) % 4];
+      p.Y = o;
+      CKL(launch_dst_pass(p, false, s), "dst pass");
+      in = o;
+      buf = (buf + 1) % 4;
+    }
+  }
+  return RSFDE_OK;
+}
+
+// y = S Lambda^{-1} S x for the spectrum kind (DSTs along every axis, scaling on the last)
+static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, double* out, cudaStream_t s) {
+  const int d = c->d;
+  const double* in = x;
+  int buf = 0;
+  for (int ax = 0; ax < d; ++ax) {
+    PassParams p = axis_params(c, ax);
+    const bool last = ax == d - 1;
+    p.X = in;
+    p.spec.kind = kind;
+    double* o = (last && d == 1) ? out : c->W[buf];
+    p.Y = o;
+    CKL(launch_dst_pass(p, last, s), "dst pass");
+    in = o;
+    buf = (buf + 1) % 4;
+  }
+  for (int ax = d - 2; ax >= 0; --ax) {
+    PassParams p = axis_params(c, ax);
+    p.X = in;
+    double* o = ax == 0 ? out : c->W[buf];
+    p.Y = o;
+    CKL(launch_dst_pass(p, false, s), "dst pass");
+    in = o;
+    buf = (buf + 1) % 4;
+  }
+  return RSFDE_OK;
+}
+
+// ------------------------------------------------------------------------------ GMRES
+static rsfde_status ensure_basis(rsfde_ctx* c, int restart) {
+  while ((int)c->V.size() < restart + 1) {
+    double* v = nullptr;
+    TRY(dalloc(c, (void**)&v, c->geo.NP * sizeof(double)));
+    c->V.push_back(v);
+  }
+  return RSFDE_OK;
+}
+
+// b^{(m)} = H E u0 - S_alpha u0 + tau F  (Eq.(tls)) into BUF (u0 = U0, F = FP)
+static rsfde_status compute_b(rsfde_ctx* c, int m, cudaStream_t s) {
+  ChainArgs a;
+  a.xmode = X_E_TIMES_R;
+  a.R = c->U0;
+  a.etafac = -1.0;
+  a.m = m;
+  a.B = c->FP;
+  a.bcoef = c->tau;
+  return oper_chain(c, a, c->BUF, s);
+}
+
+// z = K v (v = s*V): A form P_hat^{-1} A v; A~ form P_alpha^{-1} H^{-1} A v
+static rsfde_status apply_K(rsfde_ctx* c, int form, int m, const double* v, const double* vscale, double* z,
+                            cudaStream_t s) {
+  ChainArgs a;
+  a.xmode = X_E_TIMES_R;
+  a.R = v;
+  a.rscale = vscale;
+  a.m = m;
+  if (form == RSFDE_FORM_A) {
+    a.spectral = true;
+    a.spec = SPEC_PHAT;
+    return oper_chain(c, a, z, s);
+  }
+  TRY(oper_chain(c, a, c->TMP, s));
+  TRY(precond_chain(c, SPEC_HINV, c->TMP, c->TMP2, s));
+  return precond_chain(c, SPEC_PALPHA, c->TMP2, z, s);
+}
+
+// r = K-preconditioned residual of (b - A x) into out
+static rsfde_status precond_residual(rsfde_ctx* c, int form, int m, const double* b, const double* x, double* out,
+                                     cudaStream_t s) {
+  ChainArgs a;
+  a.xmode = X_E_TIMES_R;
+  a.R = x;
+  a.m = m;
+  a.ycoef = -1.0;
+  a.B = b;
+  a.bcoef = 1.0;
+  TRY(oper_chain(c, a, c->TMP, s));
+  if (form == RSFDE_FORM_A) return precond_chain(c, SPEC_PHAT, c->TMP, out, s);
+  TRY(precond_chain(c, SPEC_HINV, c->TMP, c->TMP2, s));
+  return precond_chain(c, SPEC_PALPHA, c->TMP2, out, s);
+}
+
+struct Flags {
+  int converged;
+  int breakdown;
+  double relres;
+};
+
+static rsfde_status read_flags(rsfde_ctx* c, Flags* f, cudaStream_t s) {
+  CK(cudaMemcpyAsync(c->h_flags, c->d_state, sizeof(Flags), cudaMemcpyDeviceToHost, s), "flags copy");
+  CK(cudaStreamSynchronize(s), "stream sync");
+  memcpy(f, c->h_flags, sizeof(Flags));
+  return RSFDE_OK;
+}
+
+// GMRES on K x = P^{-1} b with x = c->X on entry (x0) and exit.
+// mode_fast: first-cycle r0 = P_hat^{-1}(H FH - 2 S_alpha x0) with FH = H^{-1} tau F (valid iff
+// x0 = u^{(m)}: b - A u = tau F - 2 S_alpha u, Eq.(tls)); later cycles use b (computed on demand).
+static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b, const rsfde_gmres_cfg& cfg,
+                               cudaStream_t s, int* iters_out, double* relres_out, int* conv_out) {
+  const int restart = cfg.restart;
+  const int max_iters = cfg.max_iters > 0 ? cfg.max_iters : 10 * restart;
+  const int fixed = cfg.fixed_iters;
+  const double tol = fixed > 0 ? -1.0 : cfg.tol;
+  const int form = cfg.form;
+  TRY(ensure_basis(c, restart));
+  const long long NP = c->geo.NP;
+  const int nb = reduction_blocks(NP, kNblk);
+  int total = 0;
+  bool first = true;
+  Flags fl{0, 0, 1.0};
+  bool converged = false;
+  while (true) {
+    if (first && mode_fast && form == RSFDE_FORM_A) {
+      ChainArgs a;
+      a.xmode = X_INPUT;
+      a.Xin = c->FH;
+      a.R = c->X;
+      a.etafac = -2.0;
+      a.m = m;
+      a.spectral = true;
+      a.spec = SPEC_PHAT;
+      TRY(oper_chain(c, a, c->V[0], s));
+    } else {
+      if (!have_b) {
+        TRY(compute_b(c, m, s));
+        have_b = true;
+      }
+      TRY(precond_residual(c, form, m, c->BUF, c->X, c->V[0], s));
+    }
+    CKL(launch_sumsq(c->V[0], c->d_nrm, NP, kNblk, s), "sumsq");
+    CKL(launch_gmres_init(c->d_state, c->d_nrm, nb, c->d_vscale, first ? 1 : 0, s), "gmres init");
+    TRY(read_flags(c, &fl, s));
+    if (fl.converged) {  // r0 == 0: x0 is the solution
+      converged = true;
+      break;
+    }
+    int k = 0;
+    for (int j = 0; j < restart; ++j) {
+      const int J = j + 1;
+      TRY(apply_K(c, form, m, c->V[j], c->d_vscale + j, c->Z, s));
+      const double* const* Vp = (const double* const*)c->V.data();
+      CKL(launch_dots(Vp, c->d_vscale, J, c->Z, c->d_part, NP, kNblk, s), "dots");
+      CKL(launch_reduce(c->d_part, nb, J, c->d_h1, s), "reduce h1");
+      CKL(launch_dots_after_update(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_part, NP, kNblk, s), "dots2");
+      CKL(launch_reduce(c->d_part, nb, J, c->d_h2, s), "reduce h2");
+      CKL(launch_update_norm(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_h2, c->V[j + 1], c->d_nrm, NP, kNblk, s),
+          "update");
+      CKL(launch_arnoldi_finish(c->d_state, c->d_h1, c->d_h2, c->d_nrm, nb, j, tol, c->d_vscale + j + 1, s),
+          "finish");
+      ++total;
+      k = j + 1;
+      TRY(read_flags(c, &fl, s));
+      const bool stop = fixed > 0 ? total >= fixed : fl.converged != 0;
+      if (stop || fl.breakdown || total >= max_iters) break;
+    }
+    CKL(launch_gmres_solve_y(c->d_state, k, s), "solve y");
+    const double* const* Vp = (const double* const*)c->V.data();
+    const double* d_y = reinterpret_cast<const double*>(reinterpret_cast<const char*>(c->d_state) + offsetof(GmresState, y));
+    CKL(launch_axpy_basis(Vp, c->d_vscale, k, d_y, c->X, NP, s), "x update");
+    converged = fixed > 0 ? true : (fl.converged != 0 || fl.breakdown != 0);
+    if (converged || total >= max_iters) break;
+    first = false;
+  }
+  if (iters_out) *iters_out = total;
+  if (relres_out) *relres_out = fl.relres;
+  if (conv_out) *conv_out = converged ? 1 : 0;
+  return RSFDE_OK;
+}
+
+// ------------------------------------------------------------------------------ ABI
+extern "C" {
+
+const char* rsfde_version(void) { return "rsfde-b200 0.1 (sm_100a, FP64)"; }
+
+const char* rsfde_last_error(const rsfde_ctx* c) { return c ? c->err.c_str() : g_setup_error.c_str(); }
+
+long long rsfde_device_bytes(const rsfde_ctx* c) { return c ? c->bytes : 0; }
+
+long long rsfde_launch_count(const rsfde_ctx* c, int reset) {
+  if (!c) return 0;
+  const long long v = c->launches;
+  if (reset) const_cast<rsfde_ctx*>(c)->launches = 0;
+  return v;
+}
+
+void rsfde_destroy(rsfde_ctx* c) {
+  if (!c) return;
+  cudaDeviceSynchronize();
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->h_flags) cudaFreeHost(c->h_flags);
+  delete c;
+}
+
+static rsfde_status setup_fail(rsfde_ctx* c, rsfde_status st, const char* msg) {
+  if (msg) g_setup_error = msg;
+  else if (c) g_setup_error = c->err;
+  rsfde_destroy(c);
+  return st;
+}
+
+rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!out) return RSFDE_E_CONFIG;
+  *out = nullptr;
+  if (!p) { g_setup_error = "problem is NULL"; return RSFDE_E_CONFIG; }
+  if (p->d < 1 || p->d > 3) { g_setup_error = "d must be 1, 2 or 3"; return RSFDE_E_DIM; }
+  for (int i = 0; i < p->d; ++i) {
+    if (p->n[i] < 1 || !pow2(p->n[i] + 1) || p->n[i] + 1 > 512) {
+      g_setup_error = "n_i + 1 must be a power of two in [2, 512]";
+      return RSFDE_E_DIM;
+    }
+    if (!(p->alpha[i] > 1.0 && p->alpha[i] <= 2.0)) { g_setup_error = "alpha_i must lie in (1, 2]"; return RSFDE_E_DOMAIN; }
+    if (!(p->kappa[i] > 0.0)) { g_setup_error = "kappa_i must be > 0"; return RSFDE_E_DOMAIN; }
+  }
+  if (!(p->tau_t > 0.0) || p->M < 1) { g_setup_error = "tau_t must be > 0 and M >= 1"; return RSFDE_E_DOMAIN; }
+  if (p->e.kind == RSFDE_COEF_SEPARABLE) {
+    if (!p->e.a_half || !p->e.b_half) { g_setup_error = "separable e needs a_half and b_half"; return RSFDE_E_CONFIG; }
+  } else if (p->e.kind == RSFDE_COEF_GRID) {
+    if (!p->e.grid) { g_setup_error = "grid e needs a device grid"; return RSFDE_E_CONFIG; }
+  } else {
+    g_setup_error = "unknown coefficient kind";
+    return RSFDE_E_CONFIG;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+    g_setup_error = "no CUDA device: the rsfde library has no CPU fallback";
+    return RSFDE_E_CUDA;
+  }
+  rsfde_ctx* c = new rsfde_ctx();
+  c->d = p->d;
+  for (int i = 0; i < 3; ++i) {
+    c->n[i] = i < p->d ? p->n[i] : 1;
+    c->alpha[i] = i < p->d ? p->alpha[i] : 2.0;
+    c->kappa[i] = i < p->d ? p->kappa[i] : 0.0;
+  }
+  c->tau = p->tau_t;
+  c->M = p->M;
+  c->geo.d = c->d;
+  for (int i = 0; i < 3; ++i) c->geo.n[i] = c->n[i];
+  c->geo.P = c->n[c->d - 1] + 1;
+  long long rows = 1;
+  for (int i = 0; i < c->d - 1; ++i) rows *= c->n[i];
+  c->geo.NP = rows * c->geo.P;
+  rsfde_status st;
+  for (int i = 0; i < c->d; ++i)
+    if ((st = build_axis_tables(c, i)) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  // coefficient
+  c->ekind = p->e.kind;
+  const cudaStream_t s = S(stream);
+  const Geom& G = c->geo;
+  if (c->ekind == RSFDE_COEF_SEPARABLE) {
+    c->a_half.assign(p->e.a_half, p->e.a_half + c->M);
+    c->b_half.assign(p->e.b_half, p->e.b_half + c->M);
+    for (int i = 0; i < c->d; ++i) {
+      if (p->e.g[i] && (st = upload(c, &c->d_g[i], p->e.g[i], c->n[i])) != RSFDE_OK) return setup_fail(c, st, nullptr);
+      if (p->e.k[i] && (st = upload(c, &c->d_k[i], p->e.k[i], c->n[i])) != RSFDE_OK) return setup_fail(c, st, nullptr);
+    }
+    if ((st = upload(c, &c->d_ahalf, c->a_half.data(), c->M)) != RSFDE_OK) return setup_fail(c, st, nullptr);
+    if ((st = upload(c, &c->d_bhalf, c->b_half.data(), c->M)) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  } else {
+    c->grid = p->e.grid;
+    c->grid_static = p->e.grid_static;
+  }
+  // e-hat / e-check on the device
+  {
+    ECoef e = ecoef_at(c, 0);
+    if (c->ekind == RSFDE_COEF_GRID) e.grid = c->grid;
+    double* part = nullptr;
+    const int nblk = 148 * 4;
+    if ((st = dalloc(c, (void**)&part, 2 * nblk * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+    const int Meff = (c->ekind == RSFDE_COEF_GRID && c->grid_static) ? 1 : c->M;
+    cudaError_t ce = launch_emaxmin(e, c->d_ahalf, c->d_bhalf, Meff, c->grid_static, G, part, nblk, s);
+    if (ce != cudaSuccess) return setup_fail(c, cuda_fail(c, ce, "emaxmin"), nullptr);
+    std::vector<double> hp(2 * nblk);
+    ce = cudaMemcpyAsync(hp.data(), part, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) return setup_fail(c, cuda_fail(c, ce, "emaxmin copy"), nullptr);
+    double mx = -INFINITY, mn = INFINITY;
+    for (int b = 0; b < nblk; ++b) {
+      mx = std::fmax(mx, hp[2 * b]);
+      mn = std::fmin(mn, hp[2 * b + 1]);
+    }
+    c->ehat = mx;
+    c->echeck = mn;
+    c->ebar = 0.5 * (mx + mn);
+    if (!(mn > 0.0)) return setup_fail(c, RSFDE_E_COEFF, "e-check <= 0: e must be positive (P:33)");
+  }
+  // work memory
+  const size_t vb = (size_t)G.NP * sizeof(double);
+  double** bufs[] = {&c->W[0], &c->W[1], &c->W[2], &c->W[3], &c->Z, &c->X, &c->BUF, &c->U0, &c->FP, &c->FH, &c->TMP, &c->TMP2};
+  for (double** b : bufs)
+    if ((st = dalloc(c, (void**)b, vb)) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_vscale, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_h1, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_h2, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_part, (size_t)kNblk * 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_nrm, (size_t)kNblk * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_state, sizeof(GmresState))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if (cudaMallocHost(&c->h_flags, 64) != cudaSuccess) return setup_fail(c, RSFDE_E_NOMEM, "cudaMallocHost");
+  c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *out = c;
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_ebar(const rsfde_ctx* c, double* ebar, double* ehat, double* echeck) {
+  if (!c) return RSFDE_E_CONFIG;
+  if (ebar) *ebar = c->ebar;
+  if (ehat) *ehat = c->ehat;
+  if (echeck) *echeck = c->echeck;
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_table(const rsfde_ctx* c, int axis, int which, double* out) {
+  if (!c || !out) return RSFDE_E_CONFIG;
+  if (axis < 0 || axis >= c->d) return RSFDE_E_DIM;
+  const std::vector<double>* t = nullptr;
+  switch (which) {
+    case 0: t = &c->s_tab[axis]; break;
+    case 1: t = &c->q_tab[axis]; break;
+    case 2: t = &c->lamH_tab[axis]; break;
+    case 3: t = &c->chat_tab[axis]; break;
+    case 4: out[0] = c->eta[axis]; return RSFDE_OK;
+    default: return RSFDE_E_CONFIG;
+  }
+  memcpy(out, t->data(), t->size() * sizeof(double));
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_matvec(rsfde_ctx* c, int op, int m, const double* x, double* y, void* stream) {
+  if (!c) return RSFDE_E_CONFIG;
+  if (!x || !y || x == y) return RSFDE_E_DIM;
+  if (m < 0 || m >= c->M) return RSFDE_E_DOMAIN;
+  const cudaStream_t s = S(stream);
+  CKL(launch_pack(x, c->BUF, c->geo, s), "pack");
+  ChainArgs a;
+  a.R = c->BUF;
+  a.m = m;
+  double* res = c->Z;
+  switch (op) {
+    case RSFDE_OP_A: TRY(oper_chain(c, a, c->Z, s)); break;
+    case RSFDE_OP_ATILDE:
+      TRY(oper_chain(c, a, c->TMP2, s));
+      TRY(precond_chain(c, SPEC_HINV, c->TMP2, c->Z, s));
+      break;
+    case RSFDE_OP_S_ALPHA: a.xmode = X_ZERO; TRY(oper_chain(c, a, c->Z, s)); break;
+    case RSFDE_OP_H_ALPHA:
+      a.xmode = X_INPUT;
+      a.Xin = c->BUF;
+      a.etafac = 0.0;
+      TRY(oper_chain(c, a, c->Z, s));
+      break;
+    case RSFDE_OP_H_ALPHA_INV: TRY(precond_chain(c, SPEC_HINV, c->BUF, c->Z, s)); break;
+    case RSFDE_OP_K:
+      a.spectral = true;
+      a.spec = SPEC_PHAT;
+      TRY(oper_chain(c, a, c->Z, s));
+      break;
+    default: c->err = "unknown operator"; return RSFDE_E_CONFIG;
+  }
+  CKL(launch_unpack(res, y, c->geo, s), "unpack");
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_precond_apply(rsfde_ctx* c, int kind, const double* x, double* y, void* stream) {
+  if (!c) return RSFDE_E_CONFIG;
+  if (!x || !y || x == y) return RSFDE_E_DIM;
+  int sk;
+  switch (kind) {
+    case RSFDE_PHAT_INV: sk = SPEC_PHAT; break;
+    case RSFDE_PALPHA_INV: sk = SPEC_PALPHA; break;
+    case RSFDE_PALPHA_INV_SQRT: sk = SPEC_PALPHA_SQRT; break;
+    default: c->err = "unknown preconditioner"; return RSFDE_E_CONFIG;
+  }
+  const cudaStream_t s = S(stream);
+  CKL(launch_pack(x, c->BUF, c->geo, s), "pack");
+  TRY(precond_chain(c, sk, c->BUF, c->Z, s));
+  CKL(launch_unpack(c->Z, y, c->geo, s), "unpack");
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_compact_source(rsfde_ctx* c, const double* f_closed, double* F, void* stream) {
+  if (!c) return RSFDE_E_CONFIG;
+  if (!f_closed || !F) return RSFDE_E_DIM;
+  CKL(launch_compact_source(f_closed, F, c->geo, c->alpha, S(stream)), "compact source");
+  return RSFDE_OK;
+}
+
+static rsfde_status check_cfg(rsfde_ctx* c, const rsfde_gmres_cfg* cfg) {
+  if (!cfg || cfg->restart < 1 || cfg->restart > 50 || (cfg->fixed_iters <= 0 && !(cfg->tol >= 0.0)) ||
+      (cfg->form != RSFDE_FORM_A && cfg->form != RSFDE_FORM_ATILDE) ||
+      (cfg->x0_policy != RSFDE_X0_PREV && cfg->x0_policy != RSFDE_X0_ZERO)) {
+    c->err = "bad GMRES configuration (restart in 1..50, tol >= 0, form, x0_policy)";
+    return RSFDE_E_CONFIG;
+  }
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_gmres_step(rsfde_ctx* c, int m, const double* b, double* x, const rsfde_gmres_cfg* cfg, int* iters,
+                              double* relres, int* converged, void* stream) {
+  if (!c) return RSFDE_E_CONFIG;
+  if (!b || !x) return RSFDE_E_DIM;
+  if (m < 0 || m >= c->M) return RSFDE_E_DOMAIN;
+  TRY(check_cfg(c, cfg));
+  const cudaStream_t s = S(stream);
+  CKL(launch_pack(b, c->BUF, c->geo, s), "pack b");
+  if (cfg->x0_policy == RSFDE_X0_ZERO) CK(cudaMemsetAsync(c->X, 0, c->geo.NP * sizeof(double), s), "memset");
+  else CKL(launch_pack(x, c->X, c->geo, s), "pack x");
+  TRY(gmres_core(c, m, false, true, *cfg, s, iters, relres, converged));
+  CKL(launch_unpack(c->X, x, c->geo, s), "unpack");
+  return RSFDE_OK;
+}
+
+static bool is_host_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+// dense vector (device or host) -> padded device vector dst, staging host data through Z
+static rsfde_status load_dense(rsfde_ctx* c, const double* src, bool host, double* dst, cudaStream_t s) {
+  const long long N = (long long)c->n[0] * c->n[1] * c->n[2];
+  const double* dsrc = src;
+  if (host) {
+    CK(cudaMemcpyAsync(c->Z, src, N * sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    dsrc = c->Z;
+  }
+  CKL(launch_pack(dsrc, dst, c->geo, s), "pack");
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_solve_steps(rsfde_ctx* c, int m_begin, int m_count, double* u, const double* F, int F_static,
+                               const rsfde_gmres_cfg* cfg, rsfde_report* rep, void* stream) {
+  if (!c) return RSFDE_E_CONFIG;
+  if (!u) return RSFDE_E_DIM;
+  if (m_begin < 0 || m_count < 0 || m_begin + m_count > c->M) return RSFDE_E_DOMAIN;
+  TRY(check_cfg(c, cfg));
+  const cudaStream_t s = S(stream);
+  const long long N = (long long)c->n[0] * c->n[1] * c->n[2];
+  const size_t vb = (size_t)c->geo.NP * sizeof(double);
+  const bool u_host = is_host_ptr(u);
+  const bool f_host = F ? is_host_ptr(F) : false;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0), "event");
+  CK(cudaEventCreate(&e1), "event");
+  CK(cudaEventRecord(e0, s), "event record");
+  TRY(load_dense(c, u, u_host, c->X, s));
+  // FP = F, FH = tau H^{-1} F (first-cycle residual shortcut)
+  auto prepare_F = [&](const double* Fm) -> rsfde_status {
+    if (!Fm) {
+      CK(cudaMemsetAsync(c->FP, 0, vb, s), "memset");
+      CK(cudaMemsetAsync(c->FH, 0, vb, s), "memset");
+      return RSFDE_OK;
+    }
+    TRY(load_dense(c, Fm, f_host, c->FP, s));
+    TRY(precond_chain(c, SPEC_HINV, c->FP, c->FH, s));
+    CKL(launch_axpby(0.0, c->FH, c->tau, c->FH, c->geo.NP, s), "scale");
+    return RSFDE_OK;
+  };
+  if (!F || F_static) TRY(prepare_F(F));
+  long long total = 0;
+  bool stopped = false;
+  for (int k = 0; k < m_count; ++k) {
+    const int m = m_begin + k;
+    if (stopped) {
+      if (rep && rep->iters) rep->iters[k] = -1;
+      continue;
+    }
+    if (F && !F_static) TRY(prepare_F(F + (long long)k * N));
+    CK(cudaMemcpyAsync(c->U0, c->X, vb, cudaMemcpyDeviceToDevice, s), "copy u0");
+    int its = 0, conv = 0;
+    double rr = 0;
+    if (cfg->x0_policy == RSFDE_X0_ZERO) {
+      TRY(compute_b(c, m, s));
+      CK(cudaMemsetAsync(c->X, 0, vb, s), "memset x");
+      TRY(gmres_core(c, m, false, true, *cfg, s, &its, &rr, &conv));
+    } else {
+      TRY(gmres_core(c, m, true, false, *cfg, s, &its, &rr, &conv));
+    }
+    total += its;
+    if (rep) {
+      if (rep->iters) rep->iters[k] = its;
+      if (rep->final_relres) rep->final_relres[k] = rr;
+      if (rep->converged) rep->converged[k] = (unsigned char)conv;
+    }
+    if (!conv) stopped = true;
+  }
+  if (u_host) {
+    CKL(launch_unpack(c->X, c->Z, c->geo, s), "unpack");
+    CK(cudaMemcpyAsync(u, c->Z, N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  } else {
+    CKL(launch_unpack(c->X, u, c->geo, s), "unpack");
+  }
+  CK(cudaEventRecord(e1, s), "event record");
+  CK(cudaEventSynchronize(e1), "event sync");
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rep) {
+    rep->loop_seconds = ms * 1e-3;
+    rep->setup_seconds = c->setup_seconds;
+    rep->total_iters = total;
+  }
+  return RSFDE_OK;
+}
+
+}  // extern "C"

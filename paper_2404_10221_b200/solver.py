@@ -1,0 +1,202 @@
+"""Thin Python API over the rsfde C ABI (argument marshalling only).
+
+PyTorch provides device memory and streams; every numerical step runs in librsfde.so's
+sm_100a kernels.  Names follow the ABI (and the paper): ``matvec`` (A, A~, S_alpha, H_alpha,
+H_alpha^{-1}, K = P^{-1} A), ``precond`` (P_hat^{-1}, P_alpha^{-1}, P_alpha^{-1/2}),
+``gmres_step``, ``solve_steps``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _dp(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(L.DP)
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class RsfdeSolver:
+    """One problem (d, n, alpha, kappa, tau, M, e) set up on the current CUDA device."""
+
+    def __init__(self, d: int, n: Sequence[int], alpha: Sequence[float], kappa: Sequence[float], tau: float,
+                 M: int, a_half: np.ndarray, b_half: np.ndarray, g: Sequence[Optional[np.ndarray]],
+                 k: Sequence[Optional[np.ndarray]], stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("rsfde needs a CUDA device (no CPU fallback)")
+        self.lib = L.load()
+        self.d = d
+        self.n = tuple(int(v) for v in n)
+        self.M = M
+        self.tau = tau
+        self._keep = [np.ascontiguousarray(a_half, dtype=np.float64), np.ascontiguousarray(b_half, dtype=np.float64)]
+        prob = L.rsfde_problem()
+        prob.d = d
+        for i in range(3):
+            prob.n[i] = self.n[i] if i < d else 1
+            prob.alpha[i] = alpha[i] if i < d else 2.0
+            prob.kappa[i] = kappa[i] if i < d else 1.0
+        prob.tau_t = tau
+        prob.M = M
+        prob.e.kind = L.COEF_SEPARABLE
+        prob.e.a_half = _dp(self._keep[0])
+        prob.e.b_half = _dp(self._keep[1])
+        for i in range(3):
+            gi = g[i] if i < d else None
+            ki = k[i] if i < d else None
+            if gi is not None:
+                gi = np.ascontiguousarray(gi, dtype=np.float64)
+                self._keep.append(gi)
+            if ki is not None:
+                ki = np.ascontiguousarray(ki, dtype=np.float64)
+                self._keep.append(ki)
+            prob.e.g[i] = _dp(gi)
+            prob.e.k[i] = _dp(ki)
+        self._prob = prob
+        ctx = C.c_void_p()
+        torch.cuda.init()
+        st = self.lib.rsfde_setup(C.byref(ctx), C.byref(prob), _stream(stream))
+        if st != L.OK:
+            raise L.RsfdeError(st, self.lib.rsfde_last_error(None).decode())
+        self.ctx = ctx
+
+    @classmethod
+    def from_problem(cls, prob, stream=None) -> "RsfdeSolver":
+        """Set up from a ``paper_2404_10221_b200.inputs.Problem``."""
+        a_half, b_half, gs, ks = prob.e_tables()
+        return cls(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau, prob.M, a_half, b_half, gs, ks, stream)
+
+    # ------------------------------------------------------------------ helpers
+    def _check(self, st):
+        if st != L.OK:
+            raise L.RsfdeError(st, self.lib.rsfde_last_error(self.ctx).decode())
+
+    def _vec(self, x):
+        import torch
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64 and x.is_contiguous()):
+            raise TypeError("expected a contiguous float64 CUDA tensor")
+        if x.numel() != int(np.prod(self.n)):
+            raise ValueError(f"vector has {x.numel()} values, grid has {int(np.prod(self.n))}")
+        return x
+
+    def empty(self):
+        import torch
+        return torch.empty(self.n, dtype=torch.float64, device="cuda")
+
+    # ------------------------------------------------------------------ ABI calls
+    def matvec(self, op: int, x, m: int = 0, out=None, stream=None):
+        x = self._vec(x)
+        y = self.empty() if out is None else self._vec(out)
+        self._check(self.lib.rsfde_matvec(self.ctx, op, m, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def precond(self, kind: int, x, out=None, stream=None):
+        x = self._vec(x)
+        y = self.empty() if out is None else self._vec(out)
+        self._check(self.lib.rsfde_precond_apply(self.ctx, kind, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def compact_source(self, f_closed, out=None, stream=None):
+        """F = (prod_l calH_l f)|interior from f on the closed grid (device tensors)."""
+        import torch
+        shape = tuple(v + 2 for v in self.n)
+        if not (isinstance(f_closed, torch.Tensor) and f_closed.is_cuda and f_closed.dtype == torch.float64
+                and f_closed.is_contiguous() and tuple(f_closed.shape) == shape):
+            raise TypeError(f"expected a contiguous float64 CUDA tensor of shape {shape}")
+        y = self.empty() if out is None else self._vec(out)
+        self._check(self.lib.rsfde_compact_source(self.ctx, _ptr(f_closed), _ptr(y), _stream(stream)))
+        return y
+
+    @staticmethod
+    def cfg(restart=50, tol=1e-9, max_iters=0, x0_policy=L.X0_PREV, form=L.FORM_A, fixed_iters=0):
+        c = L.rsfde_gmres_cfg()
+        c.restart, c.tol, c.max_iters = restart, tol, max_iters
+        c.x0_policy, c.form, c.fixed_iters = x0_policy, form, fixed_iters
+        return c
+
+    def gmres_step(self, m: int, b, x, cfg, stream=None):
+        """Solve A^{(m)} x = b in place on x (x holds x_0).  Returns (iters, relres, converged)."""
+        b, x = self._vec(b), self._vec(x)
+        its, rr, conv = C.c_int(), C.c_double(), C.c_int()
+        self._check(self.lib.rsfde_gmres_step(self.ctx, m, _ptr(b), _ptr(x), C.byref(cfg), C.byref(its),
+                                              C.byref(rr), C.byref(conv), _stream(stream)))
+        return its.value, rr.value, bool(conv.value)
+
+    def solve_steps(self, u, F=None, F_static=True, m_begin=0, m_count=None, cfg=None, stream=None):
+        """March m_count CN steps in place on u (torch CUDA tensor, or numpy host array).
+
+        F: None, one static vector, or (F_static=False) m_count stacked vectors; torch CUDA
+        tensors or numpy host arrays.  Returns a report dict."""
+        m_count = self.M - m_begin if m_count is None else m_count
+        cfg = cfg or self.cfg()
+        its = (C.c_int * max(1, m_count))()
+        rr = (C.c_double * max(1, m_count))()
+        cv = (C.c_ubyte * max(1, m_count))()
+        rep = L.rsfde_report()
+        rep.iters = its
+        rep.final_relres = rr
+        rep.converged = cv
+        up = self._host_or_dev(u)
+        Fp = None if F is None else self._host_or_dev(F)
+        self._check(self.lib.rsfde_solve_steps(self.ctx, m_begin, m_count, up, Fp, 1 if F_static else 0,
+                                               C.byref(cfg), C.byref(rep), _stream(stream)))
+        return {"iters": list(its)[:m_count], "relres": list(rr)[:m_count],
+                "converged": [bool(v) for v in cv][:m_count], "loop_seconds": rep.loop_seconds,
+                "setup_seconds": rep.setup_seconds, "total_iters": rep.total_iters}
+
+    @staticmethod
+    def _host_or_dev(a):
+        if isinstance(a, np.ndarray):
+            if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+                raise TypeError("host arrays must be C-contiguous float64")
+            return C.c_void_p(a.ctypes.data)
+        import torch
+        if isinstance(a, torch.Tensor):
+            if a.dtype != torch.float64 or not a.is_contiguous():
+                raise TypeError("tensors must be contiguous float64")
+            return C.c_void_p(a.data_ptr())
+        raise TypeError("expected numpy array or torch tensor")
+
+    def ebar(self):
+        e, h, c = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.lib.rsfde_ebar(self.ctx, C.byref(e), C.byref(h), C.byref(c)))
+        return e.value, h.value, c.value
+
+    def table(self, axis: int, which: int) -> np.ndarray:
+        n = self.n[axis]
+        size = {0: n, 1: n, 2: n, 3: 2 * (n + 1), 4: 1}[which]
+        out = np.empty(size)
+        self._check(self.lib.rsfde_table(self.ctx, axis, which, out.ctypes.data_as(L.DP)))
+        return out
+
+    def launch_count(self, reset=False) -> int:
+        return int(self.lib.rsfde_launch_count(self.ctx, 1 if reset else 0))
+
+    def device_bytes(self) -> int:
+        return int(self.lib.rsfde_device_bytes(self.ctx))
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.rsfde_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): operators and preconditioners 1e-12 relative (inf-norm),
+final solutions 1e-9 relative, GMRES iteration counts within +-1.  Inputs are seeded
+uniform[-1,1] (smooth inputs cancel and are not a fair parity input, VN-9).
+"""
+import numpy as np
+import pytest
+
+from oracle import fcd, scheme
+from oracle.gmres import gmres as oracle_gmres
+from oracle.lines import LineSystem
+from paper_2404_10221_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _solver(prob):
+    from paper_2404_10221_b200.solver import RsfdeSolver
+    return RsfdeSolver.from_problem(prob)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def _host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def relerr(got, ref):
+    return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
+
+
+def _prob(kind, shape, M=4):
+    d = len(shape)
+    if kind == "c5":
+        p = I.config_c5(M=M, nn=shape if d == 3 else (3, 3, 3))
+        if d != 3:
+            p.d, p.n = d, tuple(shape)
+            p.alpha, p.kappa = (1.1, 1.5, 1.9)[:d], (1.0, 0.5, 2.0)[:d]
+            p.coeff = I.SeparableCoeff(a=lambda t: 1.5, b=lambda t: 0.5 * np.exp(-t),
+                                       g=[lambda x: np.tanh(5 * (x - 0.5))] + [None] * (d - 1), k=[None] * d)
+        return p
+    if kind == "c1":
+        return I.config_c1(n=shape[0], M=M)
+    if kind == "ex":
+        return I.example(d, shape[0], M, (1.3, 1.5, 1.7)[:d])
+    raise ValueError(kind)
+
+
+SHAPES = [("c1", (255,)), ("c1", (7,)), ("c1", (1,)), ("c5", (31, 63)), ("c5", (255, 15)),
+          ("c5", (15, 7, 31)), ("c5", (63, 63, 63)), ("ex", (3, 3, 3)), ("c5", (1, 3, 1))]
+
+
+@pytest.fixture(scope="module")
+def cache():
+    return {}
+
+
+def _setup(cache, kind, shape):
+    key = (kind, shape)
+    if key not in cache:
+        p = _prob(kind, shape)
+        cache[key] = (p, _solver(p), LineSystem(p.d, p.n, p.alpha, p.kappa, p.tau), scheme.e_bar(p)[0])
+    return cache[key]
+
+
+# ----------------------------------------------------------------------- T1 setup tables
+@pytest.mark.parametrize("kind,shape", SHAPES)
+def test_setup_tables(cache, kind, shape):
+    p, S, Ls, ebar = _setup(cache, kind, shape)
+    for i in range(p.d):
+        s = fcd.fcd_coefficients(p.alpha[i], p.n[i]).astype(float)
+        assert relerr(S.table(i, 0), s) < 1e-14
+        assert relerr(S.table(i, 1), Ls.q[i]) < 1e-14
+        assert relerr(S.table(i, 2), Ls.lamH[i]) < 1e-14
+        assert abs(S.table(i, 4)[0] - Ls.eta[i]) <= 1e-14 * Ls.eta[i]
+    eb, eh, ec = S.ebar()
+    ref = scheme.e_bar(p)
+    assert abs(eb - ref[0]) <= 4e-16 * ref[0] and abs(eh - ref[1]) <= 4e-16 * ref[1]
+
+
+# ----------------------------------------------------------------------- T3/T4 operators
+@pytest.mark.parametrize("kind,shape", SHAPES)
+@pytest.mark.parametrize("m", [0, 3])
+def test_matvec_parity(cache, kind, shape, m):
+    from paper_2404_10221_b200 import _lib as L
+    p, S, Ls, ebar = _setup(cache, kind, shape)
+    x = I.seeded_vector(1000 + m, p.n)
+    e = p.e_grid(p.t_half(m))
+    xd = _dev(x)
+    cases = {
+        L.OP_A: Ls.A(e, x),
+        L.OP_S_ALPHA: Ls.S_alpha(x),
+        L.OP_H_ALPHA: Ls.H_alpha(x),
+        L.OP_H_ALPHA_INV: Ls.H_alpha_inv(x),
+        L.OP_ATILDE: Ls.A_tilde(e, x),
+        L.OP_K: Ls.P_alpha_inv(ebar, Ls.A_tilde(e, x)),
+    }
+    for op, ref in cases.items():
+        got = _host(S.matvec(op, xd, m=m))
+        assert relerr(got, ref) < 1e-12, (op, relerr(got, ref))
+
+
+@pytest.mark.parametrize("kind,shape", SHAPES)
+def test_precond_parity(cache, kind, shape):
+    from paper_2404_10221_b200 import _lib as L
+    p, S, Ls, ebar = _setup(cache, kind, shape)
+    x = I.seeded_vector(77, p.n)
+    xd = _dev(x)
+    for kindp, ref in ((L.PHAT_INV, Ls.P_hat_inv(ebar, x)), (L.PALPHA_INV, Ls.P_alpha_inv(ebar, x)),
+                       (L.PALPHA_INV_SQRT, Ls.P_alpha_inv_sqrt(ebar, x))):
+        got = _host(S.precond(kindp, xd))
+        assert relerr(got, ref) < 1e-12, (kindp, relerr(got, ref))
+
+
+@pytest.mark.parametrize("kind,shape", SHAPES)
+def test_compact_source_parity(cache, kind, shape):
+    p, S, Ls, ebar = _setup(cache, kind, shape)
+    f = np.random.default_rng(3).uniform(-1, 1, [v + 2 for v in p.n])
+    got = _host(S.compact_source(_dev(f)))
+    assert relerr(got, scheme.compact_source(p.alpha, f)) < 1e-14
+
+
+# ----------------------------------------------------------------------- T5 one GMRES solve
+@pytest.mark.parametrize("kind,shape", [("c1", (255,)), ("c5", (31, 63)), ("c5", (15, 7, 31))])
+def test_gmres_step_parity(cache, kind, shape):
+    p, S, Ls, ebar = _setup(cache, kind, shape)
+    m = 1
+    e = p.e_grid(p.t_half(m))
+    b = I.seeded_vector(5, p.n)
+    x0 = 0.1 * I.seeded_vector(6, p.n)
+    # oracle: one-sided system P^{-1} A~ x = P^{-1} H^{-1} b (Eq.(one-sided))
+    K = lambda v: Ls.P_alpha_inv(ebar, Ls.A_tilde(e, v))
+    c = Ls.P_alpha_inv(ebar, Ls.H_alpha_inv(b))
+    ref = oracle_gmres(K, c, x0, 20, 1e-11, 200)
+    xd = _dev(x0)
+    its, rr, conv = S.gmres_step(m, _dev(b), xd, S.cfg(restart=20, tol=1e-11))
+    assert conv and abs(its - ref.iters) <= 1
+    if its != ref.iters:   # replay at matched counts
+        ref = oracle_gmres(K, c, x0, 20, 1e-11, 200, fixed_iters=its)
+    assert relerr(_host(xd), ref.x) < 1e-9
+
+
+# ----------------------------------------------------------------------- T6 time march
+def _march(prob, restart=None, tol=None, form=0, host=False):
+    from paper_2404_10221_b200 import _lib as L
+    S = _solver(prob)
+    restart = restart or prob.restart
+    tol = tol or prob.tol
+    u0 = prob.psi_interior()
+    # F^{(m+1/2)} is built on the GPU from the raw samples of f on the closed grid (inputs
+    # module), so no oracle-computed value enters the CUDA path
+    steps = [0] if prob.source_static else range(prob.M)
+    F = torch.stack([S.compact_source(_dev(prob.f_closed(prob.t_half(m)))) for m in steps])
+    Fs = bool(prob.source_static)
+    if Fs:
+        F = F[0].contiguous()
+    if host:
+        u = np.ascontiguousarray(u0)
+        rep = S.solve_steps(u, F=np.ascontiguousarray(_host(F)), F_static=Fs,
+                            cfg=S.cfg(restart=restart, tol=tol, form=form))
+        return u, rep
+    u = _dev(u0)
+    rep = S.solve_steps(u, F=F, F_static=Fs, cfg=S.cfg(restart=restart, tol=tol, form=form))
+    return _host(u), rep
+
+
+@pytest.mark.parametrize("name", ["c1", "c2s", "c4s", "c5s", "ex2"])
+def test_solve_steps_parity(name):
+    prob = {"c1": lambda: I.config_c1(n=255, M=64),
+            "c2s": lambda: I.config_c2(n=63, M=8),
+            "c4s": lambda: I.config_c4(n=31, M=4),
+            "c5s": lambda: I.config_c5(M=4, nn=(31, 15, 63)),
+            "ex2": lambda: I.example(2, 31, 16, (1.5, 1.7))}[name]()
+    u, rep = _march(prob)
+    Fst = scheme.source_F(prob, 0) if prob.source_static else None
+    uo, ro, _ = scheme.solve(prob, F_static=Fst)
+    assert all(rep["converged"]) and all(ro.converged)
+    diffs = [abs(a - b) for a, b in zip(rep["iters"], ro.iters)]
+    assert max(diffs) <= 1, (rep["iters"], ro.iters)
+    if max(diffs) > 0:
+        uo, ro, _ = scheme.solve(prob, F_static=Fst, fixed_iters=rep["iters"])
+    assert relerr(u, uo) < 1e-9, relerr(u, uo)
+
+
+def test_a_form_equals_atilde_form():
+    from paper_2404_10221_b200 import _lib as L
+    prob = I.config_c5(M=3, nn=(15, 31, 7))
+    u1, r1 = _march(prob)
+    u2, r2 = _march(prob, form=L.FORM_ATILDE)
+    assert r1["iters"] == r2["iters"]
+    assert relerr(u1, u2) < 1e-12
+
+
+def test_host_pointer_path_equals_device_path():
+    prob = I.config_c1(n=127, M=8)
+    u1, r1 = _march(prob)
+    u2, r2 = _march(prob, host=True)
+    assert r1["iters"] == r2["iters"] and np.array_equal(u1, u2)
+
+
+@pytest.mark.parametrize("shape", [(63,), (15, 31), (7, 15, 7)])
+def test_exact_preconditioner_alpha_two(shape):
+    # alpha = 2, constant e: P_hat = A exactly -> one iteration per step
+    d = len(shape)
+    prob = I.config_c5(M=3, nn=(3, 3, 3))
+    prob.d, prob.n = d, shape
+    prob.alpha, prob.kappa = (2.0,) * d, (1.0, 0.5, 2.0)[:d]
+    prob.coeff = I.SeparableCoeff(a=lambda t: 1.5, b=lambda t: 0.0, g=[None] * d, k=[None] * d)
+    prob.source = lambda xs, t: np.ones([x.size for x in xs])
+    prob.source_static = False
+    u, rep = _march(prob, restart=10, tol=1e-12)
+    assert rep["iters"] == [1, 1, 1]
+
+
+def test_zero_data_zero_iterations():
+    # f = psi = 0 -> u stays exactly 0 with no Arnoldi step
+    prob = I.config_c5(M=3, nn=(7, 7, 15))
+    prob.source = lambda xs, t: np.zeros([x.size for x in xs])
+    u, rep = _march(prob)
+    assert rep["iters"] == [0, 0, 0] and np.all(u == 0)
+
+
+def test_invalid_arguments_fail_loudly():
+    from paper_2404_10221_b200 import _lib as L
+    from paper_2404_10221_b200.solver import RsfdeSolver
+    p = I.config_c1(n=100, M=4)   # n+1 = 101 is not a power of two
+    with pytest.raises(L.RsfdeError) as ei:
+        RsfdeSolver.from_problem(p)
+    assert ei.value.status == L.E_DIM
+    p = I.config_c1(n=31, M=4)
+    p.alpha = (0.9,)
+    with pytest.raises(L.RsfdeError) as ei:
+        RsfdeSolver.from_problem(p)
+    assert ei.value.status == L.E_DOMAIN
