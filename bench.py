@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Benchmark of the tau-preconditioned GMRES hot path (arXiv 2404.10221) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C5]
+
+A *step* is one Crank-Nicolson time step of the BASELINE.json headline workload (configs[4],
+"C5": 3D 511^3, alpha=(1.1,1.5,1.9), kappa=(1,.5,2), e=1.5+0.5 tanh(5(x-1/2))e^{-t}, M=4,
+GMRES(20), tol 1e-8): the preconditioned residual and the full GMRES solve of Eq.(tls), all
+in librsfde.so kernels.  Steps cycle through m = 0..M-1 (u reset to psi = 0 at m = 0).
+
+Output: ONE JSON line on rank 0 with the metric of BASELINE.json (unknown-iterations/s =
+N * (sum of GMRES iterations) / device time; plus seconds per CN step), the e2e figure
+through the C ABI with host buffers, the live roofline of the dominant kernel class, the CPU
+oracle baseline and the SM clocks seen during the timed region.
+
+Multi-GPU (torchrun, one process per GPU): every rank solves an independent replica of the
+workload ("replicas" -- slab sharding of one grid is not built in this version, see
+DESIGN.md); value = all ranks' unknown-iterations / max-over-ranks device time, "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = None
+with open(os.path.join(ROOT, "BASELINE.json")) as _f:
+    METRIC = json.load(_f)["metric"]
+UNIT = "unknown-iterations/s"
+
+
+# ----------------------------------------------------------------------------- helpers
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(value: float, ws: int, device=None) -> float:
+    """max of a float over ranks (identity for one process)."""
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "power.draw"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[6]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def build_problem(workload: str):
+    from paper_2404_10221_b200 import inputs as I
+    if workload == "C5":
+        return I.config_c5()
+    if workload == "C4":
+        return I.config_c4()
+    if workload == "C2":
+        return I.config_c2()
+    if workload == "C1":
+        return I.config_c1()
+    if workload.startswith("C5:"):      # reduced C5 for quick runs, e.g. C5:127
+        n = int(workload.split(":")[1])
+        return I.config_c5(n=n)
+    raise ValueError(workload)
+
+
+WORKLOAD_TEXT = {
+    "C5": "C5 = BASELINE configs[4]: 3D (0,1)^3, n=511^3 (133,432,831 unknowns), alpha=(1.1,1.5,1.9), "
+          "kappa=(1,0.5,2), e=1.5+0.5*tanh(5(x-0.5))*exp(-t), M=4 CN steps, seeded uniform[-1,1] source, "
+          "GMRES(20) tol 1e-8, one-sided tau preconditioner",
+}
+
+
+# ----------------------------------------------------------------------------- CPU oracle sample
+def oracle_iteration_sample(prob, nbasis: int = 4):
+    """One GMRES iteration of the oracle (Tier L, literal one-sided system): K v = P^{-1} A~ v
+    plus modified Gram-Schmidt against ``nbasis`` basis vectors.  Returns (seconds, threads)."""
+    from oracle import scheme
+    from oracle.lines import LineSystem
+    from paper_2404_10221_b200 import inputs as I
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([int(i.get("num_threads", 1)) for i in threadpool_info()] or [os.cpu_count()])
+    except Exception:
+        threads = os.cpu_count()
+    Ls = LineSystem(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau)
+    ebar = 0.5 * (prob.e_grid(prob.t_half(0)).max() + prob.e_grid(prob.t_half(0)).min())
+    e = prob.e_grid(prob.t_half(0))
+    v = I.seeded_vector(11, prob.n)
+    V = [v / np.linalg.norm(v)] + [I.seeded_vector(12 + i, prob.n) for i in range(nbasis - 1)]
+    t0 = time.perf_counter()
+    w = Ls.P_alpha_inv(ebar, Ls.A_tilde(e, V[0]))
+    for b in V:
+        h = float(np.vdot(w, b))
+        w = w - h * b
+    nrm = float(np.linalg.norm(w))
+    _ = w / nrm
+    return time.perf_counter() - t0, threads
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    from paper_2404_10221_b200 import inputs as I
+    prob = build_problem(args.workload)
+    N = prob.N
+    small = I.config_c5(n=63)
+    for _ in range(args.warmup):
+        oracle_iteration_sample(small)
+    times = []
+    threads = os.cpu_count()
+    for _ in range(args.steps):
+        t, threads = oracle_iteration_sample(prob)
+        times.append(t)
+    tot = sum(times)
+    value = N * len(times) / tot
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": "per step: one GMRES iteration of the oracle (Tier L dense per-line "
+                                      "operators: K v = P_alpha^-1 A~ v + MGS vs 4 basis vectors) on the "
+                                      "full C5 grid"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2404_10221_b200.solver import RsfdeSolver
+
+    prob = build_problem(args.workload)
+    N = prob.N
+    t_setup = time.perf_counter()
+    S = RsfdeSolver.from_problem(prob)
+    # F (static for C3-C5) built on the device from f on the closed grid
+    steps_F = [0] if prob.source_static else list(range(prob.M))
+    Fs = [S.compact_source(torch.from_numpy(prob.f_closed(prob.t_half(m))).to(dev)) for m in steps_F]
+    u = torch.zeros(prob.n, dtype=torch.float64, device=dev)
+    u0 = torch.from_numpy(prob.psi_interior()).to(dev)
+    cfg = S.cfg(restart=prob.restart, tol=prob.tol)
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+
+    def step(i, uu, host=False):
+        m = i % prob.M
+        if m == 0:
+            if host:
+                uu[...] = u0.cpu().numpy()
+            else:
+                uu.copy_(u0)
+        F = Fs[0] if prob.source_static else Fs[m]
+        if host:
+            F = F_host if prob.source_static else F_host_steps[m]
+        rep = S.solve_steps(uu, F=F, F_static=True, m_begin=m, m_count=1, cfg=cfg)
+        if not rep["converged"][0]:
+            raise RuntimeError(f"GMRES did not converge at step m={m}: {rep}")
+        return rep["iters"][0]
+
+    for i in range(args.warmup):
+        step(i, u)
+    torch.cuda.synchronize()
+    # ---------------- device-timed region (inputs resident in HBM; vectors > L2)
+    S.profile(True)
+    S.launch_count(reset=True)
+    clocks = ClockSampler(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    iters = []
+    for i in range(args.warmup, args.warmup + args.steps):
+        iters.append(step(i, u))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    launches = S.launch_count(reset=True)
+    prof = S.profile_read()
+    S.profile(False)
+    t_dev = e0.elapsed_time(e1) * 1e-3
+    t_max = max_over_ranks(t_dev, ws, dev)
+    unk_its = sum_over_ranks(float(N * sum(iters)), ws, dev)
+    value = unk_its / t_max
+
+    # ---------------- e2e through the C ABI with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        global F_host, F_host_steps
+        F_host = Fs[0].cpu().numpy() if prob.source_static else None
+        F_host_steps = [f.cpu().numpy() for f in Fs] if not prob.source_static else None
+        pin = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+        u_host = pin.numpy()
+        pinF = torch.from_numpy(F_host).pin_memory() if F_host is not None else None
+        F_host = pinF.numpy() if pinF is not None else None
+        u_host[...] = u.cpu().numpy()
+        barrier(ws)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_iters = []
+        for i in range(args.warmup, args.warmup + args.steps):
+            e_iters.append(step(i, u_host, host=True))
+        torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, ws, dev)
+        e2e = {"value": sum_over_ranks(float(N * sum(e_iters)), ws, dev) / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(2 * N * 8), "d2h_bytes_per_step": int(N * 8),
+               "how": "rsfde_solve_steps with pinned host u and F: H2D of u and F, D2H of u inside the call, "
+                      "host wall clock around the calls after a device synchronize"}
+
+    if rank != 0:
+        return 0
+    # ---------------- roofline of the dominant kernel class
+    peak, peak_src = measured_peaks()
+    heavy = {k: v for k, v in prof.items() if k != "small" and v["ms"] > 0}
+    dom = max(heavy, key=lambda k: heavy[k]["ms"]) if heavy else None
+    roof = None
+    if dom:
+        d = prof[dom]
+        achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(args.workload, {}).get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "launches": d["launches"], "mean_launch_ms": d["ms"] / max(1, d["launches"]),
+                "algorithmic_bytes_per_launch": d["bytes"] / max(1, d["launches"])}
+    tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
+    breakdown = {k: {"share": v["ms"] / tot_ms, "ms": v["ms"], "launches": v["launches"],
+                     "GBps": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] > 0 and v["bytes"] > 0 else None}
+                 for k, v in prof.items() if v["launches"]}
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        t, threads = oracle_iteration_sample(prob)
+        cpu = {"value": N / t, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": "one GMRES iteration of the oracle on the full C5 grid (Tier L per-line dense "
+                         "operators: K v = P_alpha^-1 A~ v + MGS vs 4 basis vectors), timed once",
+               "seconds": t}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t_max / args.steps, "seconds_per_cn_step": t_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload), "n": list(prob.n),
+                   "M": prob.M, "restart": prob.restart, "tol": prob.tol, "unknowns": N,
+                   "parallelism": "replicas" if ws > 1 else "single GPU",
+                   "l2": "no flush: every vector (1.07 GB) is larger than the 126 MB L2",
+                   "iters_per_step": iters},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernel_breakdown": breakdown,
+        "cpu_baseline": cpu, "clocks": clk, "setup_seconds": setup_s,
+        "device_bytes": S.device_bytes(),
+    }
+    print(json.dumps(out), flush=True)
+    S.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+F_host = None
+F_host_steps = None
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -164,6 +164,15 @@ long long rsfde_device_bytes(const rsfde_ctx *ctx);
 /* Kernel launches issued since setup (or the last reset) -- evidence for bench.py. */
 long long rsfde_launch_count(const rsfde_ctx *ctx, int reset);
 
+/* Optional per-kernel timing: with enable != 0 every kernel launch is bracketed by CUDA events
+   on its stream and attributed to one of the classes returned by rsfde_profile_read (0 ..
+   count-1: spectral operator passes, physical operator passes, DST passes, CGS2 dots, CGS2
+   dots after update, CGS2 update+norm, solution update, small kernels).  Resets the counters
+   and returns the number of classes.  bytes = algorithmic HBM bytes (reads + writes of FP64
+   vectors) of the launches in the class. */
+int rsfde_profile(rsfde_ctx *ctx, int enable);
+int rsfde_profile_read(rsfde_ctx *ctx, int cls, long long *launches, double *ms, double *bytes, const char **name);
+
 /* Last error message of ctx (or of the last failed setup if ctx == NULL). */
 const char *rsfde_last_error(const rsfde_ctx *ctx);
 

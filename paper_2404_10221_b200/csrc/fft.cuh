@@ -90,24 +90,21 @@ __device__ __forceinline__ void idft(double2* a) {
 }
 
 // v[k1] *= W_L^{+-g k1}, k1 = 0..E-1.  tw[k] = W_L^k (exact, host long double).
-// Powers W_L^{g b}, b < 8, by recurrence from the exact W_L^g; W_L^{8 a g} loaded exactly.
+// W_L^{8 a g} is loaded exactly for every group of 8; inside a group the powers follow by
+// recurrence (<= 7 complex products, relative error <= ~2e-15), keeping only 3 complex
+// values live.
 template <int E, bool INV>
 __device__ __forceinline__ void twiddle_col(double2 (&v)[E], const double2* __restrict__ tw, int g, int L) {
   const double2 w1 = __ldg(tw + g);
-  double2 wb[8];
-  wb[0] = make_double2(1.0, 0.0);
-  wb[1] = w1;
-#pragma unroll
-  for (int b = 2; b < 8; ++b) wb[b] = c_mul(wb[b - 1], w1);
 #pragma unroll
   for (int a = 0; a < (E + 7) / 8; ++a) {
-    const double2 wa = (a == 0) ? make_double2(1.0, 0.0) : __ldg(tw + ((8 * a * g) & (L - 1)));
+    double2 w = (a == 0) ? w1 : __ldg(tw + ((8 * a * g) & (L - 1)));
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    for (int b = (a == 0 ? 1 : 0); b < 8; ++b) {
       const int k1 = 8 * a + b;
-      if (k1 == 0 || k1 >= E) continue;
-      const double2 w = (a == 0) ? wb[b] : (b == 0 ? wa : c_mul(wa, wb[b]));
+      if (k1 >= E) break;
       v[k1] = INV ? c_mulc(v[k1], w) : c_mul(v[k1], w);
+      if (b < 7) w = c_mul(w, w1);
     }
   }
 }

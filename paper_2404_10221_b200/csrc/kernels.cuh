@@ -32,6 +32,7 @@ struct Spec {
   double eta[3];
   const double* q[3];     // tau eigenvalues q_i(k), k = 1..n_i (device)
   const double* lamH[3];  // H eigenvalues (device)
+  const double* tq[3];    // eta_i q_i(k) / lambda^H_i(k) (device)
 };
 
 // first-axis source of the "X" channel of an operator pass

@@ -23,6 +23,11 @@
 //   a_1 = S_1(H_1 E v + eta_1 T_1 v), c_1 = S_1 H_1 v,
 //   a_i = S_i(H_i a_{i-1} + eta_i T_i c_{i-1}), c_i = S_i H_i c_{i-1},
 // which is exact because operators on different axes commute (Eq.(Salpha)).
+//
+// Kernel structure (v2): every kernel is a loop over FFT *phases* with ONE FFT code body
+// (small code -> no I-cache starvation, fewer live registers); per-pencil constants of
+// e(x,t) and of the spectrum are computed once per pair; stencil neighbours come from the
+// pair's shared-memory buffer instead of extra global loads.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -33,142 +38,254 @@ namespace rsfde {
 
 constexpr int kThreads = 128;
 
-struct PairInfo {
-  long long base_p, base_q;  // offset of axis position j = 1 (memory index 0) of pencils p, q
-  bool vp, vq;               // pencil exists and is not the zero pad column
-  int cp[3], cq[3];          // 0-based coordinates of the pencils (entry [axis] unused)
+enum PassMode { MODE_OPER_PHYS = 0, MODE_OPER_PHYS_LAST = 1, MODE_OPER_SPEC = 2, MODE_OPER_SPEC_LAST = 3,
+                MODE_DST = 4, MODE_DST_LAST = 5 };
+
+struct PairCtx {
+  long long off_p, off_q;  // element offset of axis position j = 1 of pencils p, q
+  long long pen_p, pen_q;  // pencil (row) index of p and q (for the per-pencil constants)
+  bool vp, vq;             // pencil exists and is not the zero pad column
+  bool vec2;               // strided axis with both pencils valid: one 16-byte access per position
 };
 
-__device__ __forceinline__ void coords_of(const PassParams& p, long long row_or_pencil, int* c) {
+// per-pencil constants of e(x,t) (separable / grid) and of the last-axis spectrum
+struct PencilConsts {
+  double eP_p, eP_q;       // prod_{i != axis} g_i(x_i) of each pencil (separable e)
+  double eK_p, eK_q;       // sum_{i != axis} k_i(x_i)
+  long long eoff_p, eoff_q;  // dense offset of position j = 1 (grid e)
+  double cH_p, cH_q;       // prod_{i != axis} lambda^H_i(k_i)      (last-axis spectrum)
+  double cP_p, cP_q;       // sum_{i != axis} eta_i q_i / lambda^H_i
+};
+
+// coordinates (0-based) of a pencil; entry [axis] = 0
+__device__ __forceinline__ void pencil_coords(const PassParams& p, long long idx, int& c0, int& c1, int& c2) {
   const Geom& G = p.geo;
-  c[0] = c[1] = c[2] = 0;
+  c0 = c1 = c2 = 0;
   if (p.contiguous) {
-    // row o over axes 0..d-2
-    long long o = row_or_pencil;
-    if (G.d == 3) { c[0] = (int)(o / G.n[1]); c[1] = (int)(o % G.n[1]); }
-    else if (G.d == 2) { c[0] = (int)o; }
+    if (G.d == 3) { c0 = (int)(idx / G.n[1]); c1 = (int)(idx % G.n[1]); }
+    else if (G.d == 2) { c0 = (int)idx; }
   } else {
-    const long long o = row_or_pencil / p.inner;
-    const long long i = row_or_pencil % p.inner;
+    const long long o = idx / p.inner;
+    const long long i = idx % p.inner;
     if (G.d == 3) {
-      if (p.axis == 0) { c[1] = (int)(i / G.P); c[2] = (int)(i % G.P); }
-      else { c[0] = (int)o; c[2] = (int)i; }
-    } else {  // d == 2, axis 0
-      c[1] = (int)i;
+      if (p.axis == 0) { c1 = (int)(i / G.P); c2 = (int)(i % G.P); }
+      else { c0 = (int)o; c2 = (int)i; }
+    } else {
+      c1 = (int)i;
     }
   }
 }
 
-__device__ __forceinline__ PairInfo pair_info(const PassParams& p, long long pair, bool active) {
-  PairInfo pi;
+__device__ __forceinline__ void pencil_consts(const PassParams& p, int c0, int c1, int c2, double& eP, double& eK,
+                                              long long& eoff, double& cH, double& cP) {
+  const int c[3] = {c0, c1, c2};
+  const Geom& G = p.geo;
+  eP = 1.0; eK = 0.0; cH = 1.0; cP = 0.0; eoff = 0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (i < G.d && i != p.axis) {
+      if (p.e.g[i]) eP *= __ldg(p.e.g[i] + c[i]);
+      if (p.e.k[i]) eK += __ldg(p.e.k[i] + c[i]);
+      if (p.spec.lamH[i]) {
+        cH *= __ldg(p.spec.lamH[i] + c[i]);
+        cP += __ldg(p.spec.tq[i] + c[i]);
+      }
+    }
+  }
+  // dense offset of (c with c[axis] = 0) for a grid coefficient
+  long long off = c[0];
+  if (G.d >= 2) off = off * G.n[1] + c[1];
+  if (G.d >= 3) off = off * G.n[2] + c[2];
+  eoff = off;
+}
+
+__device__ __forceinline__ PairCtx make_pair(const PassParams& p, long long pair, bool active) {
+  PairCtx pc;
   const Geom& G = p.geo;
   if (p.contiguous) {
     const long long rows = G.NP / G.P;
     const long long r0 = 2 * pair, r1 = 2 * pair + 1;
-    pi.base_p = r0 * G.P;
-    pi.base_q = r1 * G.P;
-    pi.vp = active && r0 < rows;
-    pi.vq = active && r1 < rows;
-    coords_of(p, r0, pi.cp);
-    coords_of(p, r1 < rows ? r1 : r0, pi.cq);
+    pc.off_p = r0 * G.P;
+    pc.off_q = r1 * G.P;
+    pc.vp = active && r0 < rows;
+    pc.vq = active && r1 < rows;
+    pc.pen_p = r0;
+    pc.pen_q = r1 < rows ? r1 : r0;
   } else {
-    const long long pen = 2 * pair;  // even pencil index, inner is even
+    const long long pen = 2 * pair;  // even pencil index; inner is even
     const long long o = pen / p.inner, i = pen % p.inner;
-    pi.base_p = o * (long long)p.n * p.inner + i;
-    pi.base_q = pi.base_p + 1;
-    coords_of(p, pen, pi.cp);
-    coords_of(p, pen + 1, pi.cq);
+    pc.off_p = o * (long long)p.n * p.inner + i;
+    pc.off_q = pc.off_p + 1;
+    pc.pen_p = pen;
+    pc.pen_q = pen + 1;
+    // the last-dimension coordinate of a strided pencil is i mod P (its pad column is P-1)
+    const int lp = (int)(i % G.P), lq = (int)((i + 1) % G.P);
     const int dl = G.d - 1;
-    pi.vp = active && pi.cp[dl] < G.n[dl];
-    pi.vq = active && pi.cq[dl] < G.n[dl];
+    pc.vp = active && lp < G.n[dl];
+    pc.vq = active && lq < G.n[dl];
   }
-  if (!pi.vp) pi.base_p = 0;
-  if (!pi.vq) pi.base_q = 0;
-  return pi;
+  if (!pc.vp) { pc.off_p = 0; pc.pen_p = 0; }
+  if (!pc.vq) { pc.off_q = 0; pc.pen_q = 0; }
+  pc.vec2 = !p.contiguous && pc.vp && pc.vq;
+  return pc;
+}
+
+__device__ __forceinline__ PencilConsts make_consts(const PassParams& p, const PairCtx& pc) {
+  PencilConsts k;
+  int a0, a1, a2, b0, b1, b2;
+  pencil_coords(p, pc.pen_p, a0, a1, a2);
+  pencil_coords(p, pc.pen_q, b0, b1, b2);
+  pencil_consts(p, a0, a1, a2, k.eP_p, k.eK_p, k.eoff_p, k.cH_p, k.cP_p);
+  pencil_consts(p, b0, b1, b2, k.eP_q, k.eK_q, k.eoff_q, k.cH_q, k.cP_q);
+  return k;
+}
+
+// prefetch the pair's rows j = g + G m (m < E/2) of X into L2
+template <int E, int G>
+__device__ __forceinline__ void prefetch_pair(const PassParams& p, const double* X, const PairCtx& pc, int g) {
+  if (!pc.vp || X == nullptr) return;
+#pragma unroll
+  for (int m = 0; m < E / 2; ++m) {
+    const int j = g + G * m;
+    if (j >= 1 && j <= p.n) {
+      const long long off = (long long)(j - 1) * p.stride;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(X + pc.off_p + off));
+      if (pc.vq && p.contiguous) asm volatile("prefetch.global.L2 [%0];" ::"l"(X + pc.off_q + off));
+    }
+  }
 }
 
 // value pair at axis position j (1..n); zero outside or for invalid pencils
-__device__ __forceinline__ double2 ld_pair(const PassParams& p, const double* __restrict__ X, const PairInfo& pi,
+__device__ __forceinline__ double2 ld_pair(const PassParams& p, const double* __restrict__ X, const PairCtx& pc,
                                            int j) {
   double2 r = make_double2(0.0, 0.0);
   if (j < 1 || j > p.n) return r;
   const long long off = (long long)(j - 1) * p.stride;
-  if (!p.contiguous && pi.vq) {
-    r = __ldg(reinterpret_cast<const double2*>(X + pi.base_p + off));
+  if (pc.vec2) {
+    r = __ldg(reinterpret_cast<const double2*>(X + pc.off_p + off));
   } else {
-    if (pi.vp) r.x = __ldg(X + pi.base_p + off);
-    if (pi.vq) r.y = __ldg(X + pi.base_q + off);
+    if (pc.vp) r.x = __ldg(X + pc.off_p + off);
+    if (pc.vq) r.y = __ldg(X + pc.off_q + off);
   }
   return r;
 }
 
-__device__ __forceinline__ void st_pair(const PassParams& p, double* X, const PairInfo& pi, int j, double2 v) {
+__device__ __forceinline__ void st_pair(const PassParams& p, double* X, const PairCtx& pc, int j, double2 v) {
   if (j < 1 || j > p.n) return;
   const long long off = (long long)(j - 1) * p.stride;
-  if (!p.contiguous && pi.vp && pi.vq) {
-    *reinterpret_cast<double2*>(X + pi.base_p + off) = v;
+  if (pc.vec2) {
+    *reinterpret_cast<double2*>(X + pc.off_p + off) = v;
   } else {
-    if (pi.vp) X[pi.base_p + off] = v.x;
-    if (pi.vq) X[pi.base_q + off] = v.y;
+    if (pc.vp) X[pc.off_p + off] = v.x;
+    if (pc.vq) X[pc.off_q + off] = v.y;
   }
 }
 
-// e(x_J, t) for the pencil with coordinates c (entry [axis] replaced by j-1)
-__device__ __forceinline__ double e_at(const PassParams& p, const int* c, int j) {
+// e(x, t) of both pencils at axis position j (1..n)
+__device__ __forceinline__ double2 e_pair(const PassParams& p, const PairCtx& pc, const PencilConsts& kc, int j) {
   const ECoef& E = p.e;
-  int cc[3] = {c[0], c[1], c[2]};
-  cc[p.axis] = j - 1;
-  const Geom& G = p.geo;
   if (E.kind == 2) {
-    long long off = cc[0];
-    if (G.d >= 2) off = off * G.n[1] + cc[1];
-    if (G.d >= 3) off = off * G.n[2] + cc[2];
-    return __ldg(E.grid + off);
+    long long st = 1;  // dense stride of the axis
+    for (int i = p.axis + 1; i < p.geo.d; ++i) st *= p.geo.n[i];
+    const long long o = (long long)(j - 1) * st;
+    return make_double2(pc.vp ? __ldg(E.grid + kc.eoff_p + o) : 0.0, pc.vq ? __ldg(E.grid + kc.eoff_q + o) : 0.0);
   }
-  double prod = 1.0, sum = 0.0;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    if (i < G.d) {
-      if (E.g[i]) prod *= __ldg(E.g[i] + cc[i]);
-      if (E.k[i]) sum += __ldg(E.k[i] + cc[i]);
-    }
-  }
-  return E.a + E.b * prod + sum;
+  const double ga = E.g[p.axis] ? __ldg(E.g[p.axis] + j - 1) : 1.0;
+  const double ka = E.k[p.axis] ? __ldg(E.k[p.axis] + j - 1) : 0.0;
+  return make_double2(fma(E.b * kc.eP_p, ga, E.a) + (kc.eK_p + ka), fma(E.b * kc.eP_q, ga, E.a) + (kc.eK_q + ka));
 }
 
-// X channel at position j: input X, or (E o R) (scaled), or 0
-__device__ __forceinline__ double2 xval(const PassParams& p, const PairInfo& pi, int j, double rs) {
-  if (j < 1 || j > p.n) return make_double2(0.0, 0.0);
-  if (p.xmode == X_INPUT) return ld_pair(p, p.X, pi, j);
-  if (p.xmode == X_ZERO) return make_double2(0.0, 0.0);
-  const double2 r = ld_pair(p, p.R, pi, j);
-  return make_double2(pi.vp ? rs * r.x * e_at(p, pi.cp, j) : 0.0, pi.vq ? rs * r.y * e_at(p, pi.cq, j) : 0.0);
-}
-
-// Lambda of the preconditioner at spectral multi-index (c with [axis] = k-1)
-__device__ __forceinline__ double spec_at(const PassParams& p, const int* c, int k) {
+// Lambda of both pencils at last-axis spectral index k (1..n)
+__device__ __forceinline__ double2 spec_pair(const PassParams& p, const PencilConsts& kc, int k) {
   const Spec& S = p.spec;
-  const int d = p.geo.d;
-  int kk[3] = {c[0], c[1], c[2]};
-  kk[p.axis] = k - 1;
-  double lamH = 1.0, lamP = S.ebar;
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    if (i < d) {
-      const double lh = __ldg(S.lamH[i] + kk[i]);
-      lamH *= lh;
-      lamP += S.eta[i] * __ldg(S.q[i] + kk[i]) / lh;
-    }
-  }
+  const double lh = __ldg(S.lamH[p.axis] + k - 1);
+  const double tq = __ldg(S.tq[p.axis] + k - 1);
+  const double lPp = S.ebar + kc.cP_p + tq, lPq = S.ebar + kc.cP_q + tq;
   switch (S.kind) {
-    case SPEC_PHAT: return lamP * lamH;
-    case SPEC_PALPHA: return lamP;
-    case SPEC_PALPHA_SQRT: return sqrt(lamP);
-    default: return lamH;
+    case SPEC_PHAT: return make_double2(lPp * (kc.cH_p * lh), lPq * (kc.cH_q * lh));
+    case SPEC_PALPHA: return make_double2(lPp, lPq);
+    case SPEC_PALPHA_SQRT: return make_double2(sqrt(lPp), sqrt(lPq));
+    default: return make_double2(kc.cH_p * lh, kc.cH_q * lh);
   }
 }
 
-// --- odd extension: v[m] (m < E/2) holds x at j = g + G m (< N); fill m >= E/2 with -x[L-j]
+// row-layout index k of register r = ri*G + k2
+template <int E, int G>
+__device__ __forceinline__ int row_k(int g, int r) {
+  constexpr int R = E / G;
+  return (g * R + r / G) + E * (r % G);
+}
+
+// ---------------------------------------------------------------------------------- FFT core
+// flip the sign of x when msk has the sign bit set (integer XOR: no FP64 pipe use)
+__device__ __forceinline__ double sgnx(double x, unsigned long long msk) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)msk);
+}
+
+// Forward (column -> row layout) or inverse (row -> column layout) FFT, E == G.
+template <int E, int G>
+__device__ __forceinline__ void fft_core(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw,
+                                         bool inv) {
+  static_assert(E == G, "fft_core: square split only (E == G)");
+  if (inv) fft_inv<E, G>(v, buf, g, tw);
+  else fft_fwd<E, G>(v, buf, g, tw);
+}
+
+// general split (E = R G, R > 1): two DFT bodies (stage sizes differ)
+template <int E, int G>
+__device__ __forceinline__ void fft_core_rect(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw,
+                                              bool inv) {
+  constexpr int R = E / G;
+  constexpr int L = E * G;
+  const unsigned long long msk = inv ? 0x8000000000000000ull : 0ull;
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, msk);
+  if (inv) {
+#pragma unroll
+    for (int ri = 0; ri < R; ++ri) dft<G>(v + ri * G);
+  } else {
+    dft<E>(v);
+  }
+  // (conj of the intermediate cancels: keep the conjugated values through the exchange and
+  //  use the forward twiddle on them, which equals conj(inverse twiddle of the true values))
+  if (!inv) twiddle_col<E, false>(v, tw, g, L);
+  __syncwarp();
+  if (!inv) {
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) buf[xidx<E, G>(k1, g)] = v[k1];
+    __syncwarp();
+#pragma unroll
+    for (int ri = 0; ri < R; ++ri)
+#pragma unroll
+      for (int t = 0; t < G; ++t) v[ri * G + t] = buf[xidx<E, G>(g * R + ri, t)];
+  } else {
+#pragma unroll
+    for (int ri = 0; ri < R; ++ri)
+#pragma unroll
+      for (int t = 0; t < G; ++t) buf[xidx<E, G>(g * R + ri, t)] = v[ri * G + t];
+    __syncwarp();
+#pragma unroll
+    for (int k1 = 0; k1 < E; ++k1) v[k1] = buf[xidx<E, G>(k1, g)];
+    twiddle_col<E, false>(v, tw, g, L);
+  }
+  if (inv) {
+    dft<E>(v);
+  } else {
+#pragma unroll
+    for (int ri = 0; ri < R; ++ri) dft<G>(v + ri * G);
+  }
+#pragma unroll
+  for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, msk);
+}
+
+template <int E, int G>
+__device__ __forceinline__ void fft_any(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw,
+                                        bool inv) {
+  if constexpr (E == G) fft_core<E, G>(v, buf, g, tw, inv);
+  else fft_core_rect<E, G>(v, buf, g, tw, inv);
+}
+
+// column layout v[m] (m < E/2) holds x at j = g + G m (< N): fill the odd extension m >= E/2
 template <int E, int G>
 __device__ __forceinline__ void odd_extend(double2 (&v)[E], double2* buf, int g) {
   constexpr int L = E * G, N = L / 2;
@@ -184,189 +301,235 @@ __device__ __forceinline__ void odd_extend(double2 (&v)[E], double2* buf, int g)
   }
 }
 
-// row-layout index helper: k of register r = ri*G + k2
-template <int E, int G>
-__device__ __forceinline__ int row_k(int g, int r) {
-  constexpr int R = E / G;
-  return (g * R + r / G) + E * (r % G);
-}
-
-// DST . Lambda^{-1} . DST on the last axis, given the first FFT's row-layout output Z of the
-// odd-extended pair.  Result (the second DST, scaled) left in row layout in v.
-template <int E, int G>
-__device__ __forceinline__ void scale_and_second_dst(const PassParams& p, const PairInfo& pi, double2 (&v)[E],
-                                                     double2* buf, int g) {
-  constexpr int L = E * G;
-  const double hs = 0.5 * p.dst_scale;
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int k = row_k<E, G>(g, r);
-    double2 w = make_double2(0.0, 0.0);
-    if (k >= 1 && k <= p.n) {
-      const double yp = -v[r].y * hs, yq = v[r].x * hs;
-      w.x = pi.vp ? yp / spec_at(p, pi.cp, k) : 0.0;
-      w.y = pi.vq ? yq / spec_at(p, pi.cq, k) : 0.0;
-    }
-    buf[k] = w;
-  }
-  __syncwarp();
-  constexpr int N = L / 2;
-#pragma unroll
-  for (int m = 0; m < E; ++m) {
-    const int j = g + G * m;
-    if (m < E / 2) {
-      v[m] = buf[j];
-    } else {
-      const double2 t = (j == N) ? make_double2(0.0, 0.0) : buf[L - j];
-      v[m] = make_double2(-t.x, -t.y);
-    }
-  }
-  fft_fwd<E, G>(v, buf, g, p.tw);
-}
-
-// store the DST result held in row layout: S x_p = -s Im Z/2, S x_q = s Re Z/2
-template <int E, int G>
-__device__ __forceinline__ void store_dst_rows(const PassParams& p, double* out, const PairInfo& pi,
-                                               const double2 (&v)[E], int g) {
-  const double hs = 0.5 * p.dst_scale;
-#pragma unroll
-  for (int r = 0; r < E; ++r) {
-    const int k = row_k<E, G>(g, r);
-    st_pair(p, out, pi, k, make_double2(-v[r].y * hs, v[r].x * hs));
-  }
-}
-
-template <int E, int G, bool SPECTRAL, bool LAST>
-__global__ void __launch_bounds__(kThreads) oper_pass_kernel(const PassParams p) {
+// ---------------------------------------------------------------------------------- the kernel
+// Each group of G threads processes one pencil pair (the loop runs once with the full grid;
+// a persistent grid with L2 prefetch of the next pair is kept behind PREFETCH but measured
+// slower).
+template <int E, int G, int MODE>
+__global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const PassParams p) {
   extern __shared__ double2 smem[];
   constexpr int L = E * G;
+  constexpr int N = L / 2;
   constexpr int GROUPS = kThreads / G;
+  constexpr bool OPER = MODE <= MODE_OPER_SPEC_LAST;
+  constexpr bool SPECTRAL = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST || MODE >= MODE_DST;
+  constexpr bool LAST = MODE == MODE_OPER_PHYS_LAST || MODE == MODE_OPER_SPEC_LAST || MODE == MODE_DST_LAST;
   const int grp = threadIdx.x / G;
   const int g = threadIdx.x % G;
   double2* buf = smem + grp * L;
-  const long long pair = (long long)blockIdx.x * GROUPS + grp;
-  const bool active = pair < p.npairs;
-  const PairInfo pi = pair_info(p, active ? pair : 0, active);
-  const double rs = p.rscale ? __ldg(p.rscale) : 1.0;
+  const double rs = (OPER && p.rscale) ? __ldg(p.rscale) : 1.0;
+  const double hs = 0.5 * p.dst_scale;
+  const double* in0 = OPER ? p.R : p.X;  // the array phase 0 reads
+  const long long gstride = (long long)gridDim.x * GROUPS;
+  constexpr bool PREFETCH = false;  // persistent + L2 prefetch measured slower (ncu r01 v3)
+  const long long iters = (p.npairs + gstride - 1) / gstride;
 
-  double2 v[E];
-  // 1. zero-padded R pair, column layout
-#pragma unroll
-  for (int m = 0; m < E; ++m) {
-    if (m < E / 2) {
-      const double2 r = ld_pair(p, p.R, pi, g + G * m);
-      v[m] = make_double2(rs * r.x, rs * r.y);
-    } else {
-      v[m] = make_double2(0.0, 0.0);
+#pragma unroll 1
+  for (long long it = 0; it < iters; ++it) {
+    const long long pair = (long long)blockIdx.x * GROUPS + grp + it * gstride;
+    const bool active = pair < p.npairs;
+    const PairCtx pc = make_pair(p, active ? pair : 0, active);
+    if (PREFETCH) {
+      const long long nxt = pair + gstride;
+      if (nxt < p.npairs) prefetch_pair<E, G>(p, in0, make_pair(p, nxt, true), g);
+      if (OPER && p.xmode == X_INPUT) prefetch_pair<E, G>(p, p.X, pc, g);
     }
-  }
-  // 2. forward FFT (conv), row layout
-  fft_fwd<E, G>(v, buf, g, p.tw);
-  // 3. C = S H R = lambda^H . S R from the zero-padded spectrum (spectral, non-last)
-  if (SPECTRAL && !LAST) {
-    __syncwarp();
+
+    double2 v[E];
+    // ---- phase-0 input
+    if (OPER) {
+      // zero-padded R pair (the Toeplitz convolution input)
 #pragma unroll
-    for (int r = 0; r < E; ++r) buf[row_k<E, G>(g, r)] = v[r];
-    __syncwarp();
-    const double hs = 0.5 * p.dst_scale;
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int k = row_k<E, G>(g, r);
-      if (k >= 1 && k <= p.n) {
-        const double2 zk = v[r], zm = buf[L - k];
-        const double f = hs * __ldg(p.lamH + k - 1);
-        st_pair(p, p.C, pi, k, make_double2(-(zk.y - zm.y) * f, (zk.x - zm.x) * f));
+      for (int m = 0; m < E; ++m) {
+        if (m < E / 2) {
+          const double2 r = ld_pair(p, p.R, pc, g + G * m);
+          v[m] = make_double2(rs * r.x, rs * r.y);
+        } else {
+          v[m] = make_double2(0.0, 0.0);
+        }
       }
+    } else {
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) v[m] = ld_pair(p, p.X, pc, g + G * m);
+      odd_extend<E, G>(v, buf, g);
     }
-  }
-  // 4. spectral multiply by c^/L and inverse FFT -> T R in column layout
+
+    // phases: OPER: 0 conv-fwd, 1 conv-inv, 2 dst(y) [, 3 second dst]; DST: 2 dst [, 3 second dst]
+    const int first = OPER ? 0 : 2;
+    const int last_phase = OPER && !SPECTRAL ? 1 : (LAST ? 3 : 2);
+#pragma unroll 1
+    for (int ph = first; ph <= last_phase; ++ph) {
+      fft_any<E, G>(v, buf, g, p.tw, ph == 1);
+      if (ph == 0) {
+        // conv forward done (row layout).  C = S H R = s lambda^H D(R) (spectral, non-last)
+        if (SPECTRAL && !LAST) {
+          __syncwarp();
 #pragma unroll
-  for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + row_k<E, G>(g, r)));
-  fft_inv<E, G>(v, buf, g, p.tw);
-  // 5. y = H X + eta T R on positions j = g + G m, m < E/2 (physical C = H R here too)
+          for (int r = 0; r < E; ++r) buf[row_k<E, G>(g, r)] = v[r];
+          __syncwarp();
 #pragma unroll
-  for (int m = 0; m < E / 2; ++m) {
-    const int j = g + G * m;
-    double2 y = make_double2(0.0, 0.0);
-    if (j >= 1 && j <= p.n) {
-      const double2 x0 = xval(p, pi, j, rs), xl = xval(p, pi, j - 1, rs), xr = xval(p, pi, j + 1, rs);
-      y.x = fma(p.hc0, x0.x, fma(p.hc1, xl.x + xr.x, p.eta * v[m].x));
-      y.y = fma(p.hc0, x0.y, fma(p.hc1, xl.y + xr.y, p.eta * v[m].y));
-      if (!SPECTRAL) {
-        if (LAST) {
-          if (p.B) {
-            const double2 b = ld_pair(p, p.B, pi, j);
-            y.x = fma(p.ycoef, y.x, p.bcoef * b.x);
-            y.y = fma(p.ycoef, y.y, p.bcoef * b.y);
-          } else {
-            y.x *= p.ycoef;
-            y.y *= p.ycoef;
+          for (int r = 0; r < E; ++r) {
+            const int k = row_k<E, G>(g, r);
+            if (k >= 1 && k <= p.n) {
+              const double2 zk = v[r], zm = buf[L - k];
+              const double f = hs * __ldg(p.lamH + k - 1);
+              st_pair(p, p.C, pc, k, make_double2(-(zk.y - zm.y) * f, (zk.x - zm.x) * f));
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + row_k<E, G>(g, r)));
+      } else if (ph == 1) {
+        // conv inverse done: column layout, T R at j = g + G m (m < E/2).
+        // X channel at j, neighbours through the shared buffer
+        const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m) {
+          const int j = g + G * m;
+          double2 x = make_double2(0.0, 0.0);
+          if (j >= 1 && j <= p.n) {
+            if (p.xmode == X_INPUT) {
+              x = ld_pair(p, p.X, pc, j);
+            } else if (p.xmode == X_E_TIMES_R) {
+              const double2 r = ld_pair(p, p.R, pc, j);
+              const double2 e = e_pair(p, pc, kc, j);
+              x = make_double2(rs * r.x * e.x, rs * r.y * e.y);
+            }
+          }
+          buf[j] = x;
+        }
+        if (g == 0) buf[N] = make_double2(0.0, 0.0);
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m) {
+          const int j = g + G * m;
+          double2 y = make_double2(0.0, 0.0);
+          if (j >= 1 && j <= p.n) {
+            const double2 xl = buf[j - 1], x0 = buf[j], xn = buf[j + 1];
+            y.x = fma(p.hc0, x0.x, fma(p.hc1, xl.x + xn.x, p.eta * v[m].x));
+            y.y = fma(p.hc0, x0.y, fma(p.hc1, xl.y + xn.y, p.eta * v[m].y));
+          }
+          v[m] = y;
+        }
+        if (!SPECTRAL) {
+          // physical outputs: Y (+ B on the last axis), C = H R (non-last)
+#pragma unroll
+          for (int m = 0; m < E / 2; ++m) {
+            const int j = g + G * m;
+            if (j >= 1 && j <= p.n) {
+              double2 y = v[m];
+              if (LAST) {
+                if (p.B) {
+                  const double2 b = ld_pair(p, p.B, pc, j);
+                  y = make_double2(fma(p.ycoef, y.x, p.bcoef * b.x), fma(p.ycoef, y.y, p.bcoef * b.y));
+                } else {
+                  y = c_scale(y, p.ycoef);
+                }
+              }
+              st_pair(p, p.Y, pc, j, y);
+            }
+          }
+          if (!LAST) {
+            // C = H R: stage R through the buffer for the neighbours
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < E / 2; ++m) {
+              const double2 r = ld_pair(p, p.R, pc, g + G * m);
+              buf[g + G * m] = make_double2(rs * r.x, rs * r.y);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < E / 2; ++m) {
+              const int j = g + G * m;
+              if (j >= 1 && j <= p.n) {
+                const double2 rl = buf[j - 1], r0 = buf[j], rn = buf[j + 1];
+                st_pair(p, p.C, pc, j, make_double2(fma(p.hc0, r0.x, p.hc1 * (rl.x + rn.x)),
+                                                    fma(p.hc0, r0.y, p.hc1 * (rl.y + rn.y))));
+              }
+            }
           }
         } else {
-          const double2 r0 = ld_pair(p, p.R, pi, j), rl = ld_pair(p, p.R, pi, j - 1), rr = ld_pair(p, p.R, pi, j + 1);
-          const double2 c = make_double2(rs * fma(p.hc0, r0.x, p.hc1 * (rl.x + rr.x)),
-                                         rs * fma(p.hc0, r0.y, p.hc1 * (rl.y + rr.y)));
-          st_pair(p, p.C, pi, j, c);
+          odd_extend<E, G>(v, buf, g);
         }
-        st_pair(p, p.Y, pi, j, y);
+      } else if (ph == 2) {
+        // first DST done (row layout): S y_p = -s Im Z/2, S y_q = s Re Z/2
+        if (!LAST) {
+#pragma unroll
+          for (int r = 0; r < E; ++r)
+            st_pair(p, p.Y, pc, row_k<E, G>(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
+        } else {
+          // Lambda^{-1} scaling, then odd extension for the second DST
+          const PencilConsts kc = make_consts(p, pc);
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < E; ++r) {
+            const int k = row_k<E, G>(g, r);
+            double2 w = make_double2(0.0, 0.0);
+            if (k >= 1 && k <= p.n) {
+              const double2 lam = spec_pair(p, kc, k);
+              w.x = pc.vp ? (-v[r].y * hs) / lam.x : 0.0;
+              w.y = pc.vq ? (v[r].x * hs) / lam.y : 0.0;
+            }
+            if (k < N) buf[k] = w;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int m = 0; m < E; ++m) {
+            const int j = g + G * m;
+            if (m < E / 2) {
+              v[m] = buf[j];
+            } else {
+              const double2 t = (j == N) ? make_double2(0.0, 0.0) : buf[L - j];
+              v[m] = make_double2(-t.x, -t.y);
+            }
+          }
+        }
+      } else {
+        // second DST done
+#pragma unroll
+        for (int r = 0; r < E; ++r)
+          st_pair(p, p.Y, pc, row_k<E, G>(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
       }
     }
-    v[m] = y;
+    __syncwarp();
   }
-  if (!SPECTRAL) return;
-  // 6. DST of y (odd extension), optionally Lambda^{-1} and the second DST
-  odd_extend<E, G>(v, buf, g);
-  fft_fwd<E, G>(v, buf, g, p.tw);
-  if (LAST) scale_and_second_dst<E, G>(p, pi, v, buf, g);
-  store_dst_rows<E, G>(p, p.Y, pi, v, g);
-}
-
-template <int E, int G, bool LAST>
-__global__ void __launch_bounds__(kThreads) dst_pass_kernel(const PassParams p) {
-  extern __shared__ double2 smem[];
-  constexpr int L = E * G;
-  constexpr int GROUPS = kThreads / G;
-  const int grp = threadIdx.x / G;
-  const int g = threadIdx.x % G;
-  double2* buf = smem + grp * L;
-  const long long pair = (long long)blockIdx.x * GROUPS + grp;
-  const bool active = pair < p.npairs;
-  const PairInfo pi = pair_info(p, active ? pair : 0, active);
-  double2 v[E];
-#pragma unroll
-  for (int m = 0; m < E / 2; ++m) v[m] = ld_pair(p, p.X, pi, g + G * m);
-  odd_extend<E, G>(v, buf, g);
-  fft_fwd<E, G>(v, buf, g, p.tw);
-  if (LAST) scale_and_second_dst<E, G>(p, pi, v, buf, g);
-  store_dst_rows<E, G>(p, p.Y, pi, v, g);
 }
 
 // ----------------------------------------------------------------------------- launchers
-template <int E, int G>
-cudaError_t launch_oper_eg(const PassParams& p, bool spectral, bool last, cudaStream_t s) {
+template <int E, int G, int MODE>
+cudaError_t launch_mode(const PassParams& p, cudaStream_t s) {
   constexpr int GROUPS = kThreads / G;
   const size_t smem = (size_t)GROUPS * E * G * sizeof(double2);
-  const long long blocks = (p.npairs + GROUPS - 1) / GROUPS;
-  void (*k)(PassParams);
-  if (spectral) k = last ? oper_pass_kernel<E, G, true, true> : oper_pass_kernel<E, G, true, false>;
-  else k = last ? oper_pass_kernel<E, G, false, true> : oper_pass_kernel<E, G, false, false>;
-  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  k<<<(unsigned)blocks, kThreads, smem, s>>>(p);
+  static int resident = 0;  // CTAs per GPU that fit at once (persistent grid)
+  if (!resident) {
+    cudaError_t err = cudaFuncSetAttribute(pass_kernel<E, G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel<E, G, MODE>, kThreads, smem);
+    if (err != cudaSuccess) return err;
+    resident = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  // one pair per group: CTAs retire and start staggered, which hides load latency better than
+  // a persistent grid did on B200 (measured), so the grid covers every pair
+  long long blocks = (p.npairs + GROUPS - 1) / GROUPS;
+  (void)resident;
+  pass_kernel<E, G, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(p);
   return cudaGetLastError();
+}
+
+template <int E, int G>
+cudaError_t launch_oper_eg(const PassParams& p, bool spectral, bool last, cudaStream_t s) {
+  if (spectral) return last ? launch_mode<E, G, MODE_OPER_SPEC_LAST>(p, s) : launch_mode<E, G, MODE_OPER_SPEC>(p, s);
+  return last ? launch_mode<E, G, MODE_OPER_PHYS_LAST>(p, s) : launch_mode<E, G, MODE_OPER_PHYS>(p, s);
 }
 
 template <int E, int G>
 cudaError_t launch_dst_eg(const PassParams& p, bool last, cudaStream_t s) {
-  constexpr int GROUPS = kThreads / G;
-  const size_t smem = (size_t)GROUPS * E * G * sizeof(double2);
-  const long long blocks = (p.npairs + GROUPS - 1) / GROUPS;
-  void (*k)(PassParams) = last ? dst_pass_kernel<E, G, true> : dst_pass_kernel<E, G, false>;
-  cudaError_t err = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  k<<<(unsigned)blocks, kThreads, smem, s>>>(p);
-  return cudaGetLastError();
+  return last ? launch_mode<E, G, MODE_DST_LAST>(p, s) : launch_mode<E, G, MODE_DST>(p, s);
 }
 
 #define RSFDE_INSTANTIATE_L(E, G)                                                                      \

@@ -17,8 +17,11 @@
 
 using namespace rsfde;
 
+#define RSFDE_NPROF 8
 namespace {
 thread_local std::string g_setup_error;
+const char* kProfNames[RSFDE_NPROF] = {"oper_pass_spectral", "oper_pass_physical", "dst_pass", "cgs_dots",
+                                       "cgs_dots2", "cgs_update_norm", "x_update", "small"};
 constexpr int kNblk = 148 * 8;
 }  // namespace
 
@@ -37,6 +40,7 @@ struct rsfde_ctx {
   double2* d_tw[3] = {nullptr, nullptr, nullptr};
   double* d_lamH[3] = {nullptr, nullptr, nullptr};
   double* d_q[3] = {nullptr, nullptr, nullptr};
+  double* d_tq[3] = {nullptr, nullptr, nullptr};
   // coefficient e
   int ekind = RSFDE_COEF_SEPARABLE;
   std::vector<double> a_half, b_half;
@@ -60,6 +64,15 @@ struct rsfde_ctx {
   double setup_seconds = 0;
   std::string err;
   std::vector<void*> allocs;
+  // optional per-launch event timing (rsfde_profile): class -> launches, ms, algorithmic bytes
+  int profiling = 0;
+  cudaStream_t prof_stream = nullptr;
+  struct Pending { int cls; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_events;
+  long long prof_launches[RSFDE_NPROF] = {0};
+  double prof_ms[RSFDE_NPROF] = {0};
+  double prof_bytes[RSFDE_NPROF] = {0};
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -74,12 +87,50 @@ static rsfde_status cuda_fail(rsfde_ctx* c, cudaError_t e, const char* what) {
     cudaError_t _e = (expr);                             \
     if (_e != cudaSuccess) return cuda_fail(c, _e, what); \
   } while (0)
-#define CKL(expr, what)                                  \
-  do {                                                   \
-    c->launches++;                                       \
-    cudaError_t _e = (expr);                             \
-    if (_e != cudaSuccess) return cuda_fail(c, _e, what); \
+static cudaEvent_t prof_event(rsfde_ctx* c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// resolve completed launch timings (call after the stream was synchronised)
+static void prof_collect(rsfde_ctx* c) {
+  for (auto& p : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) c->prof_ms[p.cls] += ms;
+    c->free_events.push_back(p.a);
+    c->free_events.push_back(p.b);
+  }
+  c->pending.clear();
+  cudaGetLastError();
+}
+
+// every kernel launch goes through LAUNCH(class, algorithmic bytes, expr, what)
+#define LAUNCH(cls, bytes, expr, what)                                   \
+  do {                                                                   \
+    c->launches++;                                                       \
+    cudaEvent_t _a = nullptr, _b = nullptr;                              \
+    if (c->profiling) {                                                  \
+      _a = prof_event(c);                                                \
+      _b = prof_event(c);                                                \
+      cudaEventRecord(_a, s);                                            \
+    }                                                                    \
+    cudaError_t _e = (expr);                                             \
+    if (_e != cudaSuccess) return cuda_fail(c, _e, what);                \
+    if (c->profiling) {                                                  \
+      cudaEventRecord(_b, s);                                            \
+      c->pending.push_back({(cls), _a, _b});                             \
+      c->prof_launches[(cls)]++;                                         \
+      c->prof_bytes[(cls)] += (double)(bytes);                           \
+    }                                                                    \
   } while (0)
+#define CKL(expr, what) LAUNCH(7, 0, expr, what)
+enum { PC_OPER_SPEC = 0, PC_OPER_PHYS = 1, PC_DST = 2, PC_DOTS = 3, PC_DOTS2 = 4, PC_UPD = 5, PC_XUPD = 6 };
 #define TRY(expr)                       \
   do {                                  \
     rsfde_status _s = (expr);           \
@@ -171,6 +222,9 @@ static rsfde_status build_axis_tables(rsfde_ctx* c, int i) {
   TRY(upload(c, &c->d_tw[i], tw.data(), L));
   TRY(upload(c, &c->d_lamH[i], c->lamH_tab[i].data(), n));
   TRY(upload(c, &c->d_q[i], c->q_tab[i].data(), n));
+  std::vector<double> tq(n);
+  for (int k = 0; k < n; ++k) tq[k] = c->eta[i] * c->q_tab[i][k] / c->lamH_tab[i][k];
+  TRY(upload(c, &c->d_tq[i], tq.data(), n));
   return RSFDE_OK;
 }
 
@@ -209,6 +263,7 @@ static PassParams axis_params(const rsfde_ctx* c, int axis) {
     p.spec.eta[i] = c->eta[i];
     p.spec.q[i] = c->d_q[i];
     p.spec.lamH[i] = c->d_lamH[i];
+    p.spec.tq[i] = c->d_tq[i];
   }
   return p;
 }
@@ -270,7 +325,12 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
       p.Y = c->W[buf];
       p.C = c->W[buf + 1];
     }
-    CKL(launch_oper_pass(p, a.spectral, last, s), "oper pass");
+    {
+      const double vb = 8.0 * (double)c->geo.NP;
+      const double nbytes = vb * (1.0 + (p.xmode == X_INPUT ? 1.0 : 0.0) + (last && p.B ? 1.0 : 0.0) +
+                                  (last ? 1.0 : 2.0));
+      LAUNCH(a.spectral ? PC_OPER_SPEC : PC_OPER_PHYS, nbytes, launch_oper_pass(p, a.spectral, last, s), "oper pass");
+    }
     if (!last) {
       Xcur = c->W[buf];
       Rcur = c->W[buf + 1];
@@ -285,7 +345,7 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
       p.X = in;
       double* o = ax == 0 ? out : c->W[(buf + 1) % 4];
       p.Y = o;
-      CKL(launch_dst_pass(p, false, s), "dst pass");
+      LAUNCH(PC_DST, 16.0 * (double)c->geo.NP, launch_dst_pass(p, false, s), "dst pass");
       in = o;
       buf = (buf + 1) % 4;
     }
@@ -305,7 +365,7 @@ static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, doubl
     p.spec.kind = kind;
     double* o = (last && d == 1) ? out : c->W[buf];
     p.Y = o;
-    CKL(launch_dst_pass(p, last, s), "dst pass");
+    LAUNCH(PC_DST, 16.0 * (double)c->geo.NP, launch_dst_pass(p, last, s), "dst pass");
     in = o;
     buf = (buf + 1) % 4;
   }
@@ -314,7 +374,7 @@ static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, doubl
     p.X = in;
     double* o = ax == 0 ? out : c->W[buf];
     p.Y = o;
-    CKL(launch_dst_pass(p, false, s), "dst pass");
+    LAUNCH(PC_DST, 16.0 * (double)c->geo.NP, launch_dst_pass(p, false, s), "dst pass");
     in = o;
     buf = (buf + 1) % 4;
   }
@@ -387,6 +447,7 @@ static rsfde_status read_flags(rsfde_ctx* c, Flags* f, cudaStream_t s) {
   CK(cudaMemcpyAsync(c->h_flags, c->d_state, sizeof(Flags), cudaMemcpyDeviceToHost, s), "flags copy");
   CK(cudaStreamSynchronize(s), "stream sync");
   memcpy(f, c->h_flags, sizeof(Flags));
+  if (c->profiling) prof_collect(c);
   return RSFDE_OK;
 }
 
@@ -437,12 +498,15 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
       const int J = j + 1;
       TRY(apply_K(c, form, m, c->V[j], c->d_vscale + j, c->Z, s));
       const double* const* Vp = (const double* const*)c->V.data();
-      CKL(launch_dots(Vp, c->d_vscale, J, c->Z, c->d_part, NP, kNblk, s), "dots");
+      const double vb = 8.0 * (double)NP;
+      LAUNCH(PC_DOTS, vb * (J + 1), launch_dots(Vp, c->d_vscale, J, c->Z, c->d_part, NP, kNblk, s), "dots");
       CKL(launch_reduce(c->d_part, nb, J, c->d_h1, s), "reduce h1");
-      CKL(launch_dots_after_update(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_part, NP, kNblk, s), "dots2");
+      LAUNCH(PC_DOTS2, vb * (J + 1), launch_dots_after_update(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_part, NP, kNblk, s),
+             "dots2");
       CKL(launch_reduce(c->d_part, nb, J, c->d_h2, s), "reduce h2");
-      CKL(launch_update_norm(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_h2, c->V[j + 1], c->d_nrm, NP, kNblk, s),
-          "update");
+      LAUNCH(PC_UPD, vb * (J + 2),
+             launch_update_norm(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_h2, c->V[j + 1], c->d_nrm, NP, kNblk, s),
+             "update");
       CKL(launch_arnoldi_finish(c->d_state, c->d_h1, c->d_h2, c->d_nrm, nb, j, tol, c->d_vscale + j + 1, s),
           "finish");
       ++total;
@@ -454,7 +518,7 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
     CKL(launch_gmres_solve_y(c->d_state, k, s), "solve y");
     const double* const* Vp = (const double* const*)c->V.data();
     const double* d_y = reinterpret_cast<const double*>(reinterpret_cast<const char*>(c->d_state) + offsetof(GmresState, y));
-    CKL(launch_axpy_basis(Vp, c->d_vscale, k, d_y, c->X, NP, s), "x update");
+    LAUNCH(PC_XUPD, 8.0 * (double)NP * (k + 2), launch_axpy_basis(Vp, c->d_vscale, k, d_y, c->X, NP, s), "x update");
     converged = fixed > 0 ? true : (fl.converged != 0 || fl.breakdown != 0);
     if (converged || total >= max_iters) break;
     first = false;
@@ -481,11 +545,37 @@ long long rsfde_launch_count(const rsfde_ctx* c, int reset) {
   return v;
 }
 
+int rsfde_profile(rsfde_ctx* c, int enable) {
+  if (!c) return -1;
+  cudaDeviceSynchronize();
+  prof_collect(c);
+  c->profiling = enable ? 1 : 0;
+  for (int i = 0; i < RSFDE_NPROF; ++i) {
+    c->prof_launches[i] = 0;
+    c->prof_ms[i] = 0;
+    c->prof_bytes[i] = 0;
+  }
+  return RSFDE_NPROF;
+}
+
+int rsfde_profile_read(rsfde_ctx* c, int cls, long long* launches, double* ms, double* bytes, const char** name) {
+  if (!c || cls < 0 || cls >= RSFDE_NPROF) return -1;
+  cudaDeviceSynchronize();
+  prof_collect(c);
+  if (launches) *launches = c->prof_launches[cls];
+  if (ms) *ms = c->prof_ms[cls];
+  if (bytes) *bytes = c->prof_bytes[cls];
+  if (name) *name = kProfNames[cls];
+  return 0;
+}
+
 void rsfde_destroy(rsfde_ctx* c) {
   if (!c) return;
   cudaDeviceSynchronize();
   for (void* p : c->allocs) cudaFree(p);
   if (c->h_flags) cudaFreeHost(c->h_flags);
+  prof_collect(c);
+  for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
   delete c;
 }
 
@@ -679,7 +769,8 @@ rsfde_status rsfde_precond_apply(rsfde_ctx* c, int kind, const double* x, double
 rsfde_status rsfde_compact_source(rsfde_ctx* c, const double* f_closed, double* F, void* stream) {
   if (!c) return RSFDE_E_CONFIG;
   if (!f_closed || !F) return RSFDE_E_DIM;
-  CKL(launch_compact_source(f_closed, F, c->geo, c->alpha, S(stream)), "compact source");
+  const cudaStream_t s = S(stream);
+  CKL(launch_compact_source(f_closed, F, c->geo, c->alpha, s), "compact source");
   return RSFDE_OK;
 }
 

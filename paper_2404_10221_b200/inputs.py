@@ -75,7 +75,7 @@ def seeded_field(seed: int, n: Sequence[int]) -> np.ndarray:
     for s in range(0, total, chunk):
         e = min(total, s + chunk)
         out[s:e] = splitmix64_uniform(seed, np.arange(s, e, dtype=np.uint64))
-    return out.reshape(n, order="F") if d > 1 else out
+    return np.ascontiguousarray(out.reshape(n, order="F")) if d > 1 else out
 
 
 def seeded_vector(seed: int, n: Sequence[int]) -> np.ndarray:

@@ -184,6 +184,22 @@ class RsfdeSolver:
         self._check(self.lib.rsfde_table(self.ctx, axis, which, out.ctypes.data_as(L.DP)))
         return out
 
+    def profile(self, enable: bool = True) -> int:
+        """Enable/disable per-launch CUDA-event timing (resets the counters)."""
+        return int(self.lib.rsfde_profile(self.ctx, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{class name: {"launches", "ms", "bytes"}} of the launches since rsfde_profile."""
+        out = {}
+        n = C.c_longlong()
+        ms, by = C.c_double(), C.c_double()
+        name = C.c_char_p()
+        cls = 0
+        while self.lib.rsfde_profile_read(self.ctx, cls, C.byref(n), C.byref(ms), C.byref(by), C.byref(name)) == 0:
+            out[name.value.decode()] = {"launches": n.value, "ms": ms.value, "bytes": by.value}
+            cls += 1
+        return out
+
     def launch_count(self, reset=False) -> int:
         return int(self.lib.rsfde_launch_count(self.ctx, 1 if reset else 0))
 
