@@ -65,7 +65,9 @@ struct PassParams {
   const double* chat;    // circulant spectrum / L, length L
   const double2* tw;     // W_L^k, length L
   const double* lamH;    // H eigenvalues of this axis (length n)
+  int flags;             // PASS_FLAG_*
 };
+enum { PASS_FLAG_NO_PIPE = 1 };
 
 // host-side launchers (pass_kernels.cu)
 cudaError_t launch_oper_pass(const PassParams& p, bool spectral, bool last, cudaStream_t s);

@@ -140,21 +140,6 @@ __device__ __forceinline__ PencilConsts make_consts(const PassParams& p, const P
   return k;
 }
 
-// prefetch the pair's rows j = g + G m (m < E/2) of X into L2
-template <int E, int G>
-__device__ __forceinline__ void prefetch_pair(const PassParams& p, const double* X, const PairCtx& pc, int g) {
-  if (!pc.vp || X == nullptr) return;
-#pragma unroll
-  for (int m = 0; m < E / 2; ++m) {
-    const int j = g + G * m;
-    if (j >= 1 && j <= p.n) {
-      const long long off = (long long)(j - 1) * p.stride;
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(X + pc.off_p + off));
-      if (pc.vq && p.contiguous) asm volatile("prefetch.global.L2 [%0];" ::"l"(X + pc.off_q + off));
-    }
-  }
-}
-
 // value pair at axis position j (1..n); zero outside or for invalid pencils
 __device__ __forceinline__ double2 ld_pair(const PassParams& p, const double* __restrict__ X, const PairCtx& pc,
                                            int j) {
@@ -302,9 +287,10 @@ __device__ __forceinline__ void odd_extend(double2 (&v)[E], double2* buf, int g)
 }
 
 // ---------------------------------------------------------------------------------- the kernel
-// Each group of G threads processes one pencil pair (the loop runs once with the full grid;
-// a persistent grid with L2 prefetch of the next pair is kept behind PREFETCH but measured
-// slower).
+// Each group of G threads processes one pencil pair; the grid covers all pairs.  (A persistent
+// grid -- with L2 prefetch, or with cp.async double buffering of the next pair -- was measured
+// slower on B200: groups drift apart, the 16-byte row pieces of neighbouring pairs stop sharing
+// L2 sectors in time and DRAM reads grow 2.7x.)
 template <int E, int G, int MODE>
 __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const PassParams p) {
   extern __shared__ double2 smem[];
@@ -319,21 +305,10 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
   double2* buf = smem + grp * L;
   const double rs = (OPER && p.rscale) ? __ldg(p.rscale) : 1.0;
   const double hs = 0.5 * p.dst_scale;
-  const double* in0 = OPER ? p.R : p.X;  // the array phase 0 reads
-  const long long gstride = (long long)gridDim.x * GROUPS;
-  constexpr bool PREFETCH = false;  // persistent + L2 prefetch measured slower (ncu r01 v3)
-  const long long iters = (p.npairs + gstride - 1) / gstride;
-
-#pragma unroll 1
-  for (long long it = 0; it < iters; ++it) {
-    const long long pair = (long long)blockIdx.x * GROUPS + grp + it * gstride;
+  {
+    const long long pair = (long long)blockIdx.x * GROUPS + grp;
     const bool active = pair < p.npairs;
     const PairCtx pc = make_pair(p, active ? pair : 0, active);
-    if (PREFETCH) {
-      const long long nxt = pair + gstride;
-      if (nxt < p.npairs) prefetch_pair<E, G>(p, in0, make_pair(p, nxt, true), g);
-      if (OPER && p.xmode == X_INPUT) prefetch_pair<E, G>(p, p.X, pc, g);
-    }
 
     double2 v[E];
     // ---- phase-0 input
@@ -369,8 +344,9 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
           __syncwarp();
 #pragma unroll
           for (int r = 0; r < E; ++r) {
+            if ((r % G) >= G / 2) continue;  // k >= N (compile-time in row layout)
             const int k = row_k<E, G>(g, r);
-            if (k >= 1 && k <= p.n) {
+            if (k >= 1) {
               const double2 zk = v[r], zm = buf[L - k];
               const double f = hs * __ldg(p.lamH + k - 1);
               st_pair(p, p.C, pc, k, make_double2(-(zk.y - zm.y) * f, (zk.x - zm.x) * f));
@@ -456,22 +432,25 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
         // first DST done (row layout): S y_p = -s Im Z/2, S y_q = s Re Z/2
         if (!LAST) {
 #pragma unroll
-          for (int r = 0; r < E; ++r)
+          for (int r = 0; r < E; ++r) {
+            if ((r % G) >= G / 2) continue;
             st_pair(p, p.Y, pc, row_k<E, G>(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
+          }
         } else {
           // Lambda^{-1} scaling, then odd extension for the second DST
           const PencilConsts kc = make_consts(p, pc);
           __syncwarp();
 #pragma unroll
           for (int r = 0; r < E; ++r) {
+            if ((r % G) >= G / 2) continue;  // only k < N feeds the odd extension
             const int k = row_k<E, G>(g, r);
             double2 w = make_double2(0.0, 0.0);
-            if (k >= 1 && k <= p.n) {
+            if (k >= 1) {
               const double2 lam = spec_pair(p, kc, k);
               w.x = pc.vp ? (-v[r].y * hs) / lam.x : 0.0;
               w.y = pc.vq ? (v[r].x * hs) / lam.y : 0.0;
             }
-            if (k < N) buf[k] = w;
+            buf[k] = w;
           }
           __syncwarp();
 #pragma unroll
@@ -488,11 +467,12 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
       } else {
         // second DST done
 #pragma unroll
-        for (int r = 0; r < E; ++r)
+        for (int r = 0; r < E; ++r) {
+          if ((r % G) >= G / 2) continue;
           st_pair(p, p.Y, pc, row_k<E, G>(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
+        }
       }
     }
-    __syncwarp();
   }
 }
 
@@ -501,22 +481,14 @@ template <int E, int G, int MODE>
 cudaError_t launch_mode(const PassParams& p, cudaStream_t s) {
   constexpr int GROUPS = kThreads / G;
   const size_t smem = (size_t)GROUPS * E * G * sizeof(double2);
-  static int resident = 0;  // CTAs per GPU that fit at once (persistent grid)
-  if (!resident) {
+  static bool attr = false;
+  if (!attr) {
     cudaError_t err = cudaFuncSetAttribute(pass_kernel<E, G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem);
     if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel<E, G, MODE>, kThreads, smem);
-    if (err != cudaSuccess) return err;
-    resident = sms * (per_sm > 0 ? per_sm : 1);
+    attr = true;
   }
-  // one pair per group: CTAs retire and start staggered, which hides load latency better than
-  // a persistent grid did on B200 (measured), so the grid covers every pair
-  long long blocks = (p.npairs + GROUPS - 1) / GROUPS;
-  (void)resident;
+  const long long blocks = (p.npairs + GROUPS - 1) / GROUPS;
   pass_kernel<E, G, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(p);
   return cudaGetLastError();
 }

@@ -8,6 +8,7 @@
 #include <cstddef>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -65,6 +66,7 @@ struct rsfde_ctx {
   std::string err;
   std::vector<void*> allocs;
   // optional per-launch event timing (rsfde_profile): class -> launches, ms, algorithmic bytes
+  int pass_flags = 0;  // PASS_FLAG_* (RSFDE_NO_PIPE=1 disables the cp.async-pipelined passes)
   int profiling = 0;
   cudaStream_t prof_stream = nullptr;
   struct Pending { int cls; cudaEvent_t a, b; };
@@ -255,6 +257,7 @@ static PassParams axis_params(const rsfde_ctx* c, int axis) {
   p.hc1 = c->alpha[axis] / 24.0;
   p.dst_scale = std::sqrt(2.0 / (double)p.N);
   p.ycoef = 1.0;
+  p.flags = c->pass_flags;
   p.chat = c->d_chat[axis];
   p.tw = c->d_tw[axis];
   p.lamH = c->d_lamH[axis];
@@ -623,6 +626,7 @@ rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) 
   }
   c->tau = p->tau_t;
   c->M = p->M;
+  if (getenv("RSFDE_NO_PIPE")) c->pass_flags |= PASS_FLAG_NO_PIPE;
   c->geo.d = c->d;
   for (int i = 0; i < 3; ++i) c->geo.n[i] = c->n[i];
   c->geo.P = c->n[c->d - 1] + 1;
