@@ -144,6 +144,8 @@ def build_problem(workload: str):
         return I.config_c5()
     if workload == "C4":
         return I.config_c4()
+    if workload == "C3":
+        return I.config_c3()
     if workload == "C2":
         return I.config_c2()
     if workload == "C1":
@@ -155,6 +157,14 @@ def build_problem(workload: str):
 
 
 WORKLOAD_TEXT = {
+    "C1": "C1 = BASELINE configs[0]: 1D n=255, alpha=1.5, kappa=1, e=1+0.5 sin(pi x) e^-t, M=64, manufactured "
+          "u=e^-t x^2(1-x)^2, GMRES(50) tol 1e-10",
+    "C2": "C2 = BASELINE configs[1]: 2D 255^2, alpha=(1.3,1.7), kappa=(1,2), e=2+xy sin t, M=32, seeded + "
+          "manufactured source, GMRES(50) tol 1e-10",
+    "C3": "C3 = BASELINE configs[2]: 2D 2047^2 (4.19M unknowns), alpha=(1.2,1.9), kappa=(1,1), "
+          "e=1+0.9 exp(-10((x-.5)^2+(y-.5)^2))(1+t), M=16, seeded source, GMRES(50) tol 1e-9",
+    "C4": "C4 = BASELINE configs[3]: 3D 255^3 (16.6M unknowns), alpha=1.5^3, kappa=1^3, "
+          "e=1+0.5 prod sin(pi x_i) cos t, M=8, seeded source, GMRES(30) tol 1e-9",
     "C5": "C5 = BASELINE configs[4]: 3D (0,1)^3, n=511^3 (133,432,831 unknowns), alpha=(1.1,1.5,1.9), "
           "kappa=(1,0.5,2), e=1.5+0.5*tanh(5(x-0.5))*exp(-t), M=4 CN steps, seeded uniform[-1,1] source, "
           "GMRES(20) tol 1e-8, one-sided tau preconditioner",

@@ -1,5 +1,6 @@
 // instantiation of the pencil-pass kernels for FFT length L = 1024
 #include "pass_kernels.cuh"
 namespace rsfde {
-RSFDE_INSTANTIATE_L(32, 32)
+using T1024 = Lay2<32, 32>;
+RSFDE_INSTANTIATE_T(T1024)
 }

@@ -1,5 +1,6 @@
 // instantiation of the pencil-pass kernels for FFT length L = 128
 #include "pass_kernels.cuh"
 namespace rsfde {
-RSFDE_INSTANTIATE_L(32, 4)
+using T128 = Lay2<32, 4>;
+RSFDE_INSTANTIATE_T(T128)
 }

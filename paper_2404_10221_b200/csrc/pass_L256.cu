@@ -1,5 +1,6 @@
 // instantiation of the pencil-pass kernels for FFT length L = 256
 #include "pass_kernels.cuh"
 namespace rsfde {
-RSFDE_INSTANTIATE_L(32, 8)
+using T256 = Lay2<32, 8>;
+RSFDE_INSTANTIATE_T(T256)
 }

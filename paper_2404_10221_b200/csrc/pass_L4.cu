@@ -1,5 +1,6 @@
 // instantiation of the pencil-pass kernels for FFT length L = 4
 #include "pass_kernels.cuh"
 namespace rsfde {
-RSFDE_INSTANTIATE_L(2, 2)
+using T4 = Lay2<2, 2>;
+RSFDE_INSTANTIATE_T(T4)
 }

@@ -1,5 +1,6 @@
 // instantiation of the pencil-pass kernels for FFT length L = 512
 #include "pass_kernels.cuh"
 namespace rsfde {
-RSFDE_INSTANTIATE_L(32, 16)
+using T512 = Lay2<32, 16>;
+RSFDE_INSTANTIATE_T(T512)
 }

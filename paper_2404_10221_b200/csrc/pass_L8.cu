@@ -1,5 +1,6 @@
 // instantiation of the pencil-pass kernels for FFT length L = 8
 #include "pass_kernels.cuh"
 namespace rsfde {
-RSFDE_INSTANTIATE_L(4, 2)
+using T8 = Lay2<4, 2>;
+RSFDE_INSTANTIATE_T(T8)
 }

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include "fft.cuh"
+#include "fft3.cuh"
 #include "kernels.cuh"
 
 namespace rsfde {
@@ -270,14 +271,44 @@ __device__ __forceinline__ void fft_any(double2 (&v)[E], double2* buf, int g, co
   else fft_core_rect<E, G>(v, buf, g, tw, inv);
 }
 
+// ---------------------------------------------------------------------------------- layouts
+// Lay2: two-stage FFT, G <= 32 threads per pair, several pairs per CTA, warp-level sync.
+template <int E_, int G_>
+struct Lay2 {
+  static constexpr int E = E_, G = G_, L = E * G, N = L / 2, GROUPS = kThreads / G, THREADS = kThreads;
+  static constexpr int MINB = E >= 32 ? 3 : 4;
+  __device__ static __forceinline__ void sync() { __syncwarp(); }
+  __device__ static __forceinline__ int rowk(int g, int r) { return row_k<E, G>(g, r); }
+  __host__ __device__ static constexpr bool lower(int r) { return (r % G) < G / 2; }
+  __device__ static __forceinline__ void fft(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw,
+                                             bool inv) {
+    fft_any<E, G>(v, buf, g, tw, inv);
+  }
+};
+// Lay3: three-stage FFT (fft3.cuh), one pair per CTA of 32 F threads, CTA-level sync.
+template <int F>
+struct Lay3 {
+  using FT = Fft3<F>;
+  static constexpr int E = FT::E, G = FT::G, L = FT::L, N = FT::N, GROUPS = 1, THREADS = FT::G;
+  static constexpr int MINB = F == 2 ? 6 : 3;
+  __device__ static __forceinline__ void sync() { __syncthreads(); }
+  __device__ static __forceinline__ int rowk(int t, int r) { return FT::rowk(t, r); }
+  __host__ __device__ static constexpr bool lower(int r) { return FT::lower(r); }
+  __device__ static __forceinline__ void fft(double2 (&v)[E], double2* buf, int t, const double2* __restrict__ tw,
+                                             bool inv) {
+    if (inv) FT::inv(v, buf, t, tw);
+    else FT::fwd(v, buf, t, tw);
+  }
+};
+
 // column layout v[m] (m < E/2) holds x at j = g + G m (< N): fill the odd extension m >= E/2
-template <int E, int G>
-__device__ __forceinline__ void odd_extend(double2 (&v)[E], double2* buf, int g) {
-  constexpr int L = E * G, N = L / 2;
-  __syncwarp();
+template <class T>
+__device__ __forceinline__ void odd_extend(double2 (&v)[T::E], double2* buf, int g) {
+  constexpr int E = T::E, G = T::G, L = T::L, N = T::N;
+  T::sync();
 #pragma unroll
   for (int m = 0; m < E / 2; ++m) buf[g + G * m] = v[m];
-  __syncwarp();
+  T::sync();
 #pragma unroll
   for (int m = E / 2; m < E; ++m) {
     const int j = g + G * m;
@@ -291,12 +322,10 @@ __device__ __forceinline__ void odd_extend(double2 (&v)[E], double2* buf, int g)
 // grid -- with L2 prefetch, or with cp.async double buffering of the next pair -- was measured
 // slower on B200: groups drift apart, the 16-byte row pieces of neighbouring pairs stop sharing
 // L2 sectors in time and DRAM reads grow 2.7x.)
-template <int E, int G, int MODE>
-__global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const PassParams p) {
+template <class T, int MODE>
+__global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassParams p) {
   extern __shared__ double2 smem[];
-  constexpr int L = E * G;
-  constexpr int N = L / 2;
-  constexpr int GROUPS = kThreads / G;
+  constexpr int E = T::E, G = T::G, L = T::L, N = T::N, GROUPS = T::GROUPS;
   constexpr bool OPER = MODE <= MODE_OPER_SPEC_LAST;
   constexpr bool SPECTRAL = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST || MODE >= MODE_DST;
   constexpr bool LAST = MODE == MODE_OPER_PHYS_LAST || MODE == MODE_OPER_SPEC_LAST || MODE == MODE_DST_LAST;
@@ -326,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
     } else {
 #pragma unroll
       for (int m = 0; m < E / 2; ++m) v[m] = ld_pair(p, p.X, pc, g + G * m);
-      odd_extend<E, G>(v, buf, g);
+      odd_extend<T>(v, buf, g);
     }
 
     // phases: OPER: 0 conv-fwd, 1 conv-inv, 2 dst(y) [, 3 second dst]; DST: 2 dst [, 3 second dst]
@@ -334,18 +363,18 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
     const int last_phase = OPER && !SPECTRAL ? 1 : (LAST ? 3 : 2);
 #pragma unroll 1
     for (int ph = first; ph <= last_phase; ++ph) {
-      fft_any<E, G>(v, buf, g, p.tw, ph == 1);
+      T::fft(v, buf, g, p.tw, ph == 1);
       if (ph == 0) {
         // conv forward done (row layout).  C = S H R = s lambda^H D(R) (spectral, non-last)
         if (SPECTRAL && !LAST) {
-          __syncwarp();
+          T::sync();
 #pragma unroll
-          for (int r = 0; r < E; ++r) buf[row_k<E, G>(g, r)] = v[r];
-          __syncwarp();
+          for (int r = 0; r < E; ++r) buf[T::rowk(g, r)] = v[r];
+          T::sync();
 #pragma unroll
           for (int r = 0; r < E; ++r) {
-            if ((r % G) >= G / 2) continue;  // k >= N (compile-time in row layout)
-            const int k = row_k<E, G>(g, r);
+            if (!T::lower(r)) continue;  // k >= N (compile-time in row layout)
+            const int k = T::rowk(g, r);
             if (k >= 1) {
               const double2 zk = v[r], zm = buf[L - k];
               const double f = hs * __ldg(p.lamH + k - 1);
@@ -354,12 +383,12 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
           }
         }
 #pragma unroll
-        for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + row_k<E, G>(g, r)));
+        for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
       } else if (ph == 1) {
         // conv inverse done: column layout, T R at j = g + G m (m < E/2).
         // X channel at j, neighbours through the shared buffer
         const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
-        __syncwarp();
+        T::sync();
 #pragma unroll
         for (int m = 0; m < E / 2; ++m) {
           const int j = g + G * m;
@@ -376,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
           buf[j] = x;
         }
         if (g == 0) buf[N] = make_double2(0.0, 0.0);
-        __syncwarp();
+        T::sync();
 #pragma unroll
         for (int m = 0; m < E / 2; ++m) {
           const int j = g + G * m;
@@ -408,13 +437,13 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
           }
           if (!LAST) {
             // C = H R: stage R through the buffer for the neighbours
-            __syncwarp();
+            T::sync();
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const double2 r = ld_pair(p, p.R, pc, g + G * m);
               buf[g + G * m] = make_double2(rs * r.x, rs * r.y);
             }
-            __syncwarp();
+            T::sync();
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const int j = g + G * m;
@@ -426,24 +455,24 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
             }
           }
         } else {
-          odd_extend<E, G>(v, buf, g);
+          odd_extend<T>(v, buf, g);
         }
       } else if (ph == 2) {
         // first DST done (row layout): S y_p = -s Im Z/2, S y_q = s Re Z/2
         if (!LAST) {
 #pragma unroll
           for (int r = 0; r < E; ++r) {
-            if ((r % G) >= G / 2) continue;
-            st_pair(p, p.Y, pc, row_k<E, G>(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
+            if (!T::lower(r)) continue;
+            st_pair(p, p.Y, pc, T::rowk(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
           }
         } else {
           // Lambda^{-1} scaling, then odd extension for the second DST
           const PencilConsts kc = make_consts(p, pc);
-          __syncwarp();
+          T::sync();
 #pragma unroll
           for (int r = 0; r < E; ++r) {
-            if ((r % G) >= G / 2) continue;  // only k < N feeds the odd extension
-            const int k = row_k<E, G>(g, r);
+            if (!T::lower(r)) continue;  // only k < N feeds the odd extension
+            const int k = T::rowk(g, r);
             double2 w = make_double2(0.0, 0.0);
             if (k >= 1) {
               const double2 lam = spec_pair(p, kc, k);
@@ -452,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
             }
             buf[k] = w;
           }
-          __syncwarp();
+          T::sync();
 #pragma unroll
           for (int m = 0; m < E; ++m) {
             const int j = g + G * m;
@@ -468,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
         // second DST done
 #pragma unroll
         for (int r = 0; r < E; ++r) {
-          if ((r % G) >= G / 2) continue;
-          st_pair(p, p.Y, pc, row_k<E, G>(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
+          if (!T::lower(r)) continue;
+          st_pair(p, p.Y, pc, T::rowk(g, r), make_double2(-v[r].y * hs, v[r].x * hs));
         }
       }
     }
@@ -477,35 +506,33 @@ __global__ void __launch_bounds__(kThreads, E >= 32 ? 3 : 4) pass_kernel(const P
 }
 
 // ----------------------------------------------------------------------------- launchers
-template <int E, int G, int MODE>
+template <class T, int MODE>
 cudaError_t launch_mode(const PassParams& p, cudaStream_t s) {
-  constexpr int GROUPS = kThreads / G;
-  const size_t smem = (size_t)GROUPS * E * G * sizeof(double2);
+  const size_t smem = (size_t)T::GROUPS * T::L * sizeof(double2);
   static bool attr = false;
   if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(pass_kernel<E, G, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
+    cudaError_t err = cudaFuncSetAttribute(pass_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     attr = true;
   }
-  const long long blocks = (p.npairs + GROUPS - 1) / GROUPS;
-  pass_kernel<E, G, MODE><<<(unsigned)blocks, kThreads, smem, s>>>(p);
+  const long long blocks = (p.npairs + T::GROUPS - 1) / T::GROUPS;
+  pass_kernel<T, MODE><<<(unsigned)blocks, T::THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 
-template <int E, int G>
-cudaError_t launch_oper_eg(const PassParams& p, bool spectral, bool last, cudaStream_t s) {
-  if (spectral) return last ? launch_mode<E, G, MODE_OPER_SPEC_LAST>(p, s) : launch_mode<E, G, MODE_OPER_SPEC>(p, s);
-  return last ? launch_mode<E, G, MODE_OPER_PHYS_LAST>(p, s) : launch_mode<E, G, MODE_OPER_PHYS>(p, s);
+template <class T>
+cudaError_t launch_oper_t(const PassParams& p, bool spectral, bool last, cudaStream_t s) {
+  if (spectral) return last ? launch_mode<T, MODE_OPER_SPEC_LAST>(p, s) : launch_mode<T, MODE_OPER_SPEC>(p, s);
+  return last ? launch_mode<T, MODE_OPER_PHYS_LAST>(p, s) : launch_mode<T, MODE_OPER_PHYS>(p, s);
 }
 
-template <int E, int G>
-cudaError_t launch_dst_eg(const PassParams& p, bool last, cudaStream_t s) {
-  return last ? launch_mode<E, G, MODE_DST_LAST>(p, s) : launch_mode<E, G, MODE_DST>(p, s);
+template <class T>
+cudaError_t launch_dst_t(const PassParams& p, bool last, cudaStream_t s) {
+  return last ? launch_mode<T, MODE_DST_LAST>(p, s) : launch_mode<T, MODE_DST>(p, s);
 }
 
-#define RSFDE_INSTANTIATE_L(E, G)                                                                      \
-  template cudaError_t launch_oper_eg<E, G>(const PassParams&, bool, bool, cudaStream_t);             \
-  template cudaError_t launch_dst_eg<E, G>(const PassParams&, bool, cudaStream_t);
+#define RSFDE_INSTANTIATE_T(T)                                                             \
+  template cudaError_t launch_oper_t<T>(const PassParams&, bool, bool, cudaStream_t);     \
+  template cudaError_t launch_dst_t<T>(const PassParams&, bool, cudaStream_t);
 
 }  // namespace rsfde

@@ -596,8 +596,8 @@ rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) 
   if (!p) { g_setup_error = "problem is NULL"; return RSFDE_E_CONFIG; }
   if (p->d < 1 || p->d > 3) { g_setup_error = "d must be 1, 2 or 3"; return RSFDE_E_DIM; }
   for (int i = 0; i < p->d; ++i) {
-    if (p->n[i] < 1 || !pow2(p->n[i] + 1) || p->n[i] + 1 > 512) {
-      g_setup_error = "n_i + 1 must be a power of two in [2, 512]";
+    if (p->n[i] < 1 || !pow2(p->n[i] + 1) || p->n[i] + 1 > 2048) {
+      g_setup_error = "n_i + 1 must be a power of two in [2, 2048]";
       return RSFDE_E_DIM;
     }
     if (!(p->alpha[i] > 1.0 && p->alpha[i] <= 2.0)) { g_setup_error = "alpha_i must lie in (1, 2]"; return RSFDE_E_DOMAIN; }

@@ -53,7 +53,9 @@ def _prob(kind, shape, M=4):
 
 
 SHAPES = [("c1", (255,)), ("c1", (7,)), ("c1", (1,)), ("c5", (31, 63)), ("c5", (255, 15)),
-          ("c5", (15, 7, 31)), ("c5", (63, 63, 63)), ("ex", (3, 3, 3)), ("c5", (1, 3, 1))]
+          ("c5", (15, 7, 31)), ("c5", (63, 63, 63)), ("ex", (3, 3, 3)), ("c5", (1, 3, 1)),
+          # long pencils: the three-stage FFT (L = 2048, 4096), strided and contiguous axes
+          ("c5", (2047, 7)), ("c5", (7, 2047)), ("c5", (3, 1023, 3)), ("c1", (2047,))]
 
 
 @pytest.fixture(scope="module")
@@ -170,9 +172,10 @@ def _march(prob, restart=None, tol=None, form=0, host=False):
     return _host(u), rep
 
 
-@pytest.mark.parametrize("name", ["c1", "c2s", "c4s", "c5s", "ex2"])
+@pytest.mark.parametrize("name", ["c1", "c2s", "c3s", "c4s", "c5s", "ex2"])
 def test_solve_steps_parity(name):
     prob = {"c1": lambda: I.config_c1(n=255, M=64),
+            "c3s": lambda: _c3_small(),
             "c2s": lambda: I.config_c2(n=63, M=8),
             "c4s": lambda: I.config_c4(n=31, M=4),
             "c5s": lambda: I.config_c5(M=4, nn=(31, 15, 63)),
@@ -186,6 +189,14 @@ def test_solve_steps_parity(name):
     if max(diffs) > 0:
         uo, ro, _ = scheme.solve(prob, F_static=Fst, fixed_iters=rep["iters"])
     assert relerr(u, uo) < 1e-9, relerr(u, uo)
+
+
+def _c3_small():
+    # C3's coefficients and orders on a 2047 x 63 grid (long contiguous-axis FFT), 3 steps
+    p = I.config_c3(n=63, M=3)
+    p.n = (63, 2047)
+    p.source = lambda xs, t: I._interior_embed(I.seeded_field(p.seed, p.n))
+    return p
 
 
 def test_a_form_equals_atilde_form():
