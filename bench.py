@@ -13,9 +13,11 @@ N * (sum of GMRES iterations) / device time; plus seconds per CN step), the e2e 
 through the C ABI with host buffers, the live roofline of the dominant kernel class, the CPU
 oracle baseline and the SM clocks seen during the timed region.
 
-Multi-GPU (torchrun, one process per GPU): every rank solves an independent replica of the
-workload ("replicas" -- slab sharding of one grid is not built in this version, see
-DESIGN.md); value = all ranks' unknown-iterations / max-over-ranks device time, "weak".
+Multi-GPU (torchrun, one process per GPU, N > 1): the 3D grid is slab-sharded along x_1 over the
+N ranks (rsfde_team_*: NCCL all-to-all transposes for the x_1 transforms, allreduce of the CGS2
+dots) -- strong scaling of the same problem; value = N_unknowns * iterations / max-over-ranks
+device time.  If the sharded setup fails (NCCL unavailable) the ranks fall back to independent
+replicas ("weak") and the JSON line says so.
 """
 from __future__ import annotations
 
@@ -375,6 +377,101 @@ F_host = None
 F_host_steps = None
 
 
+def run_sharded(args):
+    """N > 1: one C5 grid slab-sharded along x_1 over the ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = _dist()
+    dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2404_10221_b200.solver import RsfdeSolver, RsfdeTeam
+    prob = build_problem(args.workload)
+    if prob.d != 3 or (prob.n[0] + 1) % ws or (prob.n[1] + 1) % ws:
+        raise RuntimeError("sharding needs a 3D grid with N | n1+1 and N | n2+1")
+    obj = [RsfdeTeam.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    t_setup = time.perf_counter()
+    T = RsfdeTeam(prob, nranks=ws, rank=rank, nlocal=1, nccl_id=obj[0])
+    lo, cnt = T.slab()
+    f = prob.f_closed(prob.t_half(0))
+    F = T.compact_source(torch.from_numpy(np.ascontiguousarray(f[lo:lo + cnt + 2])).to(dev))
+    del f
+    u = torch.zeros((cnt, prob.n[1], prob.n[2]), dtype=torch.float64, device=dev)
+    cfg = RsfdeSolver.cfg(restart=prob.restart, tol=prob.tol)
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+
+    def step(i, uu):
+        m = i % prob.M
+        if m == 0:
+            uu.zero_()
+        rep = T.solve_steps(uu, F=F, F_static=True, m_begin=m, m_count=1, cfg=cfg)
+        if not rep["converged"][0]:
+            raise RuntimeError(f"GMRES did not converge at step m={m}: {rep}")
+        return rep["iters"][0]
+
+    for i in range(args.warmup):
+        step(i, u)
+    T.launch_count(reset=True)
+    clocks = ClockSampler(local)
+    barrier(ws)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    iters = [step(i, u) for i in range(args.warmup, args.warmup + args.steps)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clk = clocks.stop()
+    launches = T.launch_count(reset=True)
+    t_max = max_over_ranks(e0.elapsed_time(e1) * 1e-3, ws, dev)
+    N = prob.N
+    value = N * sum(iters) / t_max
+    e2e = None
+    if not args.no_e2e:
+        u_host = torch.zeros((cnt, prob.n[1], prob.n[2]), dtype=torch.float64).pin_memory()
+        F_host = F.cpu().pin_memory()
+        Fd = torch.empty_like(F)
+        barrier(ws)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_iters = []
+        for i in range(args.warmup, args.warmup + args.steps):
+            u.copy_(u_host, non_blocking=True)
+            Fd.copy_(F_host, non_blocking=True)
+            m = i % prob.M
+            if m == 0:
+                u.zero_()
+            rep = T.solve_steps(u, F=Fd, F_static=True, m_begin=m, m_count=1, cfg=cfg)
+            e_iters.append(rep["iters"][0])
+            u_host.copy_(u, non_blocking=True)
+            torch.cuda.synchronize()
+        t_e2e = max_over_ranks(time.perf_counter() - t0, ws, dev)
+        e2e = {"value": N * sum(e_iters) / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(float(2 * u.numel() * 8), ws, dev)),
+               "d2h_bytes_per_step": int(sum_over_ranks(float(u.numel() * 8), ws, dev)),
+               "how": "per rank: H2D of its slab of u and F from pinned memory, rsfde_team_solve_steps, D2H of u"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps,
+            "seconds_per_cn_step": t_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload), "n": list(prob.n),
+                       "M": prob.M, "restart": prob.restart, "tol": prob.tol, "unknowns": N,
+                       "parallelism": f"slab x1 over {ws} ranks (NCCL all-to-all transposes, allreduce dots)",
+                       "l2": "no flush: every slab vector exceeds L2 at N <= 8 for C5", "iters_per_step": iters},
+            "e2e": e2e, "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "clocks": clk,
+            "setup_seconds": setup_s,
+        }
+        print(json.dumps(out), flush=True)
+    T.close()
+    dist.destroy_process_group()
+    return 0
+
+
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -384,9 +481,19 @@ def main(argv=None):
     ap.add_argument("--workload", default="C5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent replicas instead of sharding")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
+    ws = _dist()[0]
+    if ws > 1 and not args.replicas:
+        try:
+            return run_sharded(args)
+        except Exception as exc:  # NCCL / sharding unavailable: independent replicas instead
+            print(f"sharded run failed ({exc!r}); falling back to replicas", file=sys.stderr, flush=True)
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.destroy_process_group()
     return run_ours(args)
 
 

@@ -173,6 +173,38 @@ long long rsfde_launch_count(const rsfde_ctx *ctx, int reset);
 int rsfde_profile(rsfde_ctx *ctx, int enable);
 int rsfde_profile_read(rsfde_ctx *ctx, int cls, long long *launches, double *ms, double *bytes, const char **name);
 
+/* ------------------------------------------------------------------------------------------
+ * Slab-sharded 3D solver.  The grid is split along x_1 over nranks ranks (x_1 padded
+ * to n_1+1, so nranks must divide n_1+1 and n_2+1; the pad plane is the DST-I zero).  Operator
+ * passes along x_3 and x_2 run on the x_1-slabs; the fused DST . Lambda^{-1} . DST pass along x_1
+ * runs after an all-to-all transpose to x_2-slabs (x_1 contiguous); CGS2 dots are allreduced.
+ * nccl_id != NULL (nlocal must be 1): one rank per process, transport = NCCL (id from
+ *             rsfde_nccl_unique_id on rank 0, broadcast by the caller; nranks = 1 is allowed and
+ *             exercises the NCCL path on one GPU); vectors are the rank's slab x_1 in [x1_lo, x1_lo+count)
+ *             (rsfde_team_slab), dense C layout [x_1 local][x_2][x_3].
+ * nccl_id == NULL, nlocal = nranks: all ranks emulated in this process on one device (transport =
+ *             device copies);
+ *             vectors are the whole dense grid.  Used by the single-GPU parity tests.
+ * Same conventions as above otherwise (device pointers, stream-ordered, A form only). */
+typedef struct rsfde_team rsfde_team;
+rsfde_status rsfde_nccl_unique_id(void *out128);
+rsfde_status rsfde_team_setup(rsfde_team **out, const rsfde_problem *p, int nranks, int rank, int nlocal,
+                              const void *nccl_id, void *stream);
+rsfde_status rsfde_team_slab(const rsfde_team *t, int local, int *x1_lo, int *x1_count);
+/* op: RSFDE_OP_K (P_hat^{-1} A) or RSFDE_OP_A */
+rsfde_status rsfde_team_matvec(rsfde_team *t, int op, int m, const double *x, double *y, void *stream);
+rsfde_status rsfde_team_precond_apply(rsfde_team *t, int kind, const double *x, double *y, void *stream);
+rsfde_status rsfde_team_solve_steps(rsfde_team *t, int m_begin, int m_count, double *u, const double *F,
+                                    int F_static, const rsfde_gmres_cfg *cfg, rsfde_report *rep, void *stream);
+/* F on the local slab of local rank `local` from f on the closed slab x_1 in [x1_lo-1, x1_lo+count],
+   x_2, x_3 closed (count+2, n_2+2, n_3+2 values, dense) -- the compact stencil of
+   rsfde_compact_source restricted to the slab. */
+rsfde_status rsfde_team_compact_source(rsfde_team *t, int local, const double *f_closed_slab, double *F_slab,
+                                       void *stream);
+long long rsfde_team_launch_count(const rsfde_team *t, int reset);
+const char *rsfde_team_last_error(const rsfde_team *t);
+void rsfde_team_destroy(rsfde_team *t);
+
 /* Last error message of ctx (or of the last failed setup if ctx == NULL). */
 const char *rsfde_last_error(const rsfde_ctx *ctx);
 

@@ -65,6 +65,18 @@ SIGNATURES = {
     "rsfde_last_error": (C.c_char_p, [C.c_void_p]),
     "rsfde_destroy": (None, [C.c_void_p]),
     "rsfde_version": (C.c_char_p, []),
+    "rsfde_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "rsfde_team_setup": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(rsfde_problem), C.c_int, C.c_int, C.c_int,
+                                   C.c_void_p, C.c_void_p]),
+    "rsfde_team_slab": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "rsfde_team_matvec": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rsfde_team_precond_apply": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rsfde_team_solve_steps": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
+                                         C.POINTER(rsfde_gmres_cfg), C.POINTER(rsfde_report), C.c_void_p]),
+    "rsfde_team_launch_count": (C.c_longlong, [C.c_void_p, C.c_int]),
+    "rsfde_team_compact_source": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rsfde_team_last_error": (C.c_char_p, [C.c_void_p]),
+    "rsfde_team_destroy": (None, [C.c_void_p]),
 }
 
 _lib = None

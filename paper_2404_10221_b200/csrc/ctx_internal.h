@@ -1,0 +1,76 @@
+// Internal (not part of the ABI): the context structure shared by the single-GPU host code
+// (rsfde_host.cu) and the slab-sharded module (rsfde_shard.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/rsfde.h"
+#include "kernels.cuh"
+
+#define RSFDE_NPROF 8
+
+using rsfde::Geom;
+using rsfde::GmresState;
+
+struct rsfde_ctx {
+  int d = 0;
+  int n[3] = {1, 1, 1};
+  double alpha[3] = {2, 2, 2}, kappa[3] = {0, 0, 0};
+  double tau = 0;
+  int M = 0;
+  Geom geo{};
+  double eta[3] = {0, 0, 0};
+  // host copies of the 1-D tables (long double computed, FP64 stored)
+  std::vector<double> s_tab[3], q_tab[3], lamH_tab[3], chat_tab[3];
+  // device tables
+  double* d_chat[3] = {nullptr, nullptr, nullptr};
+  double2* d_tw[3] = {nullptr, nullptr, nullptr};
+  double* d_lamH[3] = {nullptr, nullptr, nullptr};
+  double* d_q[3] = {nullptr, nullptr, nullptr};
+  double* d_tq[3] = {nullptr, nullptr, nullptr};
+  // coefficient e
+  int ekind = RSFDE_COEF_SEPARABLE;
+  std::vector<double> a_half, b_half;
+  double* d_g[3] = {nullptr, nullptr, nullptr};
+  double* d_k[3] = {nullptr, nullptr, nullptr};
+  double *d_ahalf = nullptr, *d_bhalf = nullptr;
+  const double* grid = nullptr;
+  int grid_static = 0;
+  double ebar = 0, ehat = 0, echeck = 0;
+  // work vectors (padded layout, zero pads)
+  double* W[4] = {nullptr, nullptr, nullptr, nullptr};
+  double *Z = nullptr, *X = nullptr, *BUF = nullptr, *U0 = nullptr, *FP = nullptr, *FH = nullptr;
+  double *TMP = nullptr, *TMP2 = nullptr;
+  std::vector<double*> V;
+  double* d_vscale = nullptr;
+  double *d_h1 = nullptr, *d_h2 = nullptr, *d_part = nullptr, *d_nrm = nullptr;
+  GmresState* d_state = nullptr;
+  void* h_flags = nullptr;  // pinned 16 bytes: converged, breakdown, relres
+  long long bytes = 0;
+  long long launches = 0;
+  double setup_seconds = 0;
+  std::string err;
+  std::vector<void*> allocs;
+  // optional per-launch event timing (rsfde_profile): class -> launches, ms, algorithmic bytes
+  int pass_flags = 0;  // PASS_FLAG_* (RSFDE_NO_PIPE=1 disables the cp.async-pipelined passes)
+  int profiling = 0;
+  cudaStream_t prof_stream = nullptr;
+  struct Pending {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> free_events;
+  long long prof_launches[RSFDE_NPROF] = {0};
+  double prof_ms[RSFDE_NPROF] = {0};
+  double prof_bytes[RSFDE_NPROF] = {0};
+};
+
+
+// setup without the work vectors / basis (tables, e-bar only)
+extern "C" rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void* stream, bool alloc_work);
+// pass parameters of one axis of the context's (unsharded) grid
+rsfde::PassParams rsfde_axis_params(const rsfde_ctx* c, int axis);
+rsfde::ECoef rsfde_ecoef_at(const rsfde_ctx* c, int m);

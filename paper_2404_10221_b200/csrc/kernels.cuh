@@ -66,6 +66,11 @@ struct PassParams {
   const double2* tw;     // W_L^k, length L
   const double* lamH;    // H eigenvalues of this axis (length n)
   int flags;             // PASS_FLAG_*
+  // global coordinates of this (possibly sharded / transposed) grid: axis i of the local array
+  // starts at global index coff[i] of a physical axis with cext[i] interior points; pencils whose
+  // global coordinate on a non-pass axis is >= cext are zero pads (never stored)
+  int coff[3];
+  int cext[3];
 };
 enum { PASS_FLAG_NO_PIPE = 1 };
 

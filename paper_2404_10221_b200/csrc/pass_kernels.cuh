@@ -79,7 +79,7 @@ __device__ __forceinline__ void pencil_coords(const PassParams& p, long long idx
 
 __device__ __forceinline__ void pencil_consts(const PassParams& p, int c0, int c1, int c2, double& eP, double& eK,
                                               long long& eoff, double& cH, double& cP) {
-  const int c[3] = {c0, c1, c2};
+  const int c[3] = {c0 + p.coff[0], c1 + p.coff[1], c2 + p.coff[2]};  // global coordinates
   const Geom& G = p.geo;
   eP = 1.0; eK = 0.0; cH = 1.0; cP = 0.0; eoff = 0;
 #pragma unroll
@@ -93,25 +93,38 @@ __device__ __forceinline__ void pencil_consts(const PassParams& p, int c0, int c
       }
     }
   }
-  // dense offset of (c with c[axis] = 0) for a grid coefficient
-  long long off = c[0];
-  if (G.d >= 2) off = off * G.n[1] + c[1];
-  if (G.d >= 3) off = off * G.n[2] + c[2];
+  // dense offset of (c with c[axis] = 0) for a grid coefficient (unsharded grids only)
+  long long off = c0;
+  if (G.d >= 2) off = off * G.n[1] + c1;
+  if (G.d >= 3) off = off * G.n[2] + c2;
   eoff = off;
+}
+
+// pencil inside the global grid on every non-pass axis?
+__device__ __forceinline__ bool pencil_inside(const PassParams& p, int c0, int c1, int c2) {
+  const int c[3] = {c0, c1, c2};
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (i < p.geo.d && i != p.axis) ok = ok && (c[i] + p.coff[i] < p.cext[i]);
+  return ok;
 }
 
 __device__ __forceinline__ PairCtx make_pair(const PassParams& p, long long pair, bool active) {
   PairCtx pc;
   const Geom& G = p.geo;
+  int a0, a1, a2, b0, b1, b2;
   if (p.contiguous) {
     const long long rows = G.NP / G.P;
     const long long r0 = 2 * pair, r1 = 2 * pair + 1;
     pc.off_p = r0 * G.P;
     pc.off_q = r1 * G.P;
-    pc.vp = active && r0 < rows;
-    pc.vq = active && r1 < rows;
     pc.pen_p = r0;
     pc.pen_q = r1 < rows ? r1 : r0;
+    pencil_coords(p, pc.pen_p, a0, a1, a2);
+    pencil_coords(p, pc.pen_q, b0, b1, b2);
+    pc.vp = active && r0 < rows && pencil_inside(p, a0, a1, a2);
+    pc.vq = active && r1 < rows && pencil_inside(p, b0, b1, b2);
   } else {
     const long long pen = 2 * pair;  // even pencil index; inner is even
     const long long o = pen / p.inner, i = pen % p.inner;
@@ -119,11 +132,10 @@ __device__ __forceinline__ PairCtx make_pair(const PassParams& p, long long pair
     pc.off_q = pc.off_p + 1;
     pc.pen_p = pen;
     pc.pen_q = pen + 1;
-    // the last-dimension coordinate of a strided pencil is i mod P (its pad column is P-1)
-    const int lp = (int)(i % G.P), lq = (int)((i + 1) % G.P);
-    const int dl = G.d - 1;
-    pc.vp = active && lp < G.n[dl];
-    pc.vq = active && lq < G.n[dl];
+    pencil_coords(p, pen, a0, a1, a2);
+    pencil_coords(p, pen + 1, b0, b1, b2);
+    pc.vp = active && pencil_inside(p, a0, a1, a2);
+    pc.vq = active && pencil_inside(p, b0, b1, b2);
   }
   if (!pc.vp) { pc.off_p = 0; pc.pen_p = 0; }
   if (!pc.vq) { pc.off_q = 0; pc.pen_q = 0; }

@@ -13,69 +13,16 @@
 #include <string>
 #include <vector>
 
-#include "../../include/rsfde.h"
-#include "kernels.cuh"
+#include "ctx_internal.h"
 
 using namespace rsfde;
 
-#define RSFDE_NPROF 8
 namespace {
 thread_local std::string g_setup_error;
 const char* kProfNames[RSFDE_NPROF] = {"oper_pass_spectral", "oper_pass_physical", "dst_pass", "cgs_dots",
                                        "cgs_dots2", "cgs_update_norm", "x_update", "small"};
 constexpr int kNblk = 148 * 8;
 }  // namespace
-
-struct rsfde_ctx {
-  int d = 0;
-  int n[3] = {1, 1, 1};
-  double alpha[3] = {2, 2, 2}, kappa[3] = {0, 0, 0};
-  double tau = 0;
-  int M = 0;
-  Geom geo{};
-  double eta[3] = {0, 0, 0};
-  // host copies of the 1-D tables (long double computed, FP64 stored)
-  std::vector<double> s_tab[3], q_tab[3], lamH_tab[3], chat_tab[3];
-  // device tables
-  double* d_chat[3] = {nullptr, nullptr, nullptr};
-  double2* d_tw[3] = {nullptr, nullptr, nullptr};
-  double* d_lamH[3] = {nullptr, nullptr, nullptr};
-  double* d_q[3] = {nullptr, nullptr, nullptr};
-  double* d_tq[3] = {nullptr, nullptr, nullptr};
-  // coefficient e
-  int ekind = RSFDE_COEF_SEPARABLE;
-  std::vector<double> a_half, b_half;
-  double* d_g[3] = {nullptr, nullptr, nullptr};
-  double* d_k[3] = {nullptr, nullptr, nullptr};
-  double *d_ahalf = nullptr, *d_bhalf = nullptr;
-  const double* grid = nullptr;
-  int grid_static = 0;
-  double ebar = 0, ehat = 0, echeck = 0;
-  // work vectors (padded layout, zero pads)
-  double* W[4] = {nullptr, nullptr, nullptr, nullptr};
-  double *Z = nullptr, *X = nullptr, *BUF = nullptr, *U0 = nullptr, *FP = nullptr, *FH = nullptr;
-  double *TMP = nullptr, *TMP2 = nullptr;
-  std::vector<double*> V;
-  double* d_vscale = nullptr;
-  double *d_h1 = nullptr, *d_h2 = nullptr, *d_part = nullptr, *d_nrm = nullptr;
-  GmresState* d_state = nullptr;
-  void* h_flags = nullptr;  // pinned 16 bytes: converged, breakdown, relres
-  long long bytes = 0;
-  long long launches = 0;
-  double setup_seconds = 0;
-  std::string err;
-  std::vector<void*> allocs;
-  // optional per-launch event timing (rsfde_profile): class -> launches, ms, algorithmic bytes
-  int pass_flags = 0;  // PASS_FLAG_* (RSFDE_NO_PIPE=1 disables the cp.async-pipelined passes)
-  int profiling = 0;
-  cudaStream_t prof_stream = nullptr;
-  struct Pending { int cls; cudaEvent_t a, b; };
-  std::vector<Pending> pending;
-  std::vector<cudaEvent_t> free_events;
-  long long prof_launches[RSFDE_NPROF] = {0};
-  double prof_ms[RSFDE_NPROF] = {0};
-  double prof_bytes[RSFDE_NPROF] = {0};
-};
 
 // ------------------------------------------------------------------------------ helpers
 static rsfde_status cuda_fail(rsfde_ctx* c, cudaError_t e, const char* what) {
@@ -231,7 +178,7 @@ static rsfde_status build_axis_tables(rsfde_ctx* c, int i) {
 }
 
 // ------------------------------------------------------------------------------ passes
-static PassParams axis_params(const rsfde_ctx* c, int axis) {
+PassParams rsfde_axis_params(const rsfde_ctx* c, int axis) {
   PassParams p;
   memset(&p, 0, sizeof p);
   p.geo = c->geo;
@@ -261,6 +208,10 @@ static PassParams axis_params(const rsfde_ctx* c, int axis) {
   p.chat = c->d_chat[axis];
   p.tw = c->d_tw[axis];
   p.lamH = c->d_lamH[axis];
+  for (int i = 0; i < 3; ++i) {
+    p.coff[i] = 0;
+    p.cext[i] = c->n[i];
+  }
   p.spec.ebar = c->ebar;
   for (int i = 0; i < 3; ++i) {
     p.spec.eta[i] = c->eta[i];
@@ -271,7 +222,7 @@ static PassParams axis_params(const rsfde_ctx* c, int axis) {
   return p;
 }
 
-static ECoef ecoef_at(const rsfde_ctx* c, int m) {
+ECoef rsfde_ecoef_at(const rsfde_ctx* c, int m) {
   ECoef e;
   memset(&e, 0, sizeof e);
   if (c->ekind == RSFDE_COEF_GRID) {
@@ -311,13 +262,13 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
   int buf = 0;
   for (int ax = 0; ax < d; ++ax) {
     const bool last = ax == d - 1;
-    PassParams p = axis_params(c, ax);
+    PassParams p = rsfde_axis_params(c, ax);
     p.xmode = ax == 0 ? a.xmode : X_INPUT;
     p.X = Xcur;
     p.R = Rcur;
     p.rscale = ax == 0 ? a.rscale : nullptr;
     p.eta = a.etafac * c->eta[ax];
-    if (ax == 0 && a.xmode == X_E_TIMES_R) p.e = ecoef_at(c, a.m);
+    if (ax == 0 && a.xmode == X_E_TIMES_R) p.e = rsfde_ecoef_at(c, a.m);
     p.spec.kind = a.spec;
     if (last) {
       p.Y = (a.spectral && d > 1) ? c->W[buf] : out;
@@ -344,7 +295,7 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
     // inverse DSTs along axes d-2 .. 0
     const double* in = c->W[buf];
     for (int ax = d - 2; ax >= 0; --ax) {
-      PassParams p = axis_params(c, ax);
+      PassParams p = rsfde_axis_params(c, ax);
       p.X = in;
       double* o = ax == 0 ? out : c->W[(buf + 1) % 4];
       p.Y = o;
@@ -362,7 +313,7 @@ static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, doubl
   const double* in = x;
   int buf = 0;
   for (int ax = 0; ax < d; ++ax) {
-    PassParams p = axis_params(c, ax);
+    PassParams p = rsfde_axis_params(c, ax);
     const bool last = ax == d - 1;
     p.X = in;
     p.spec.kind = kind;
@@ -373,7 +324,7 @@ static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, doubl
     buf = (buf + 1) % 4;
   }
   for (int ax = d - 2; ax >= 0; --ax) {
-    PassParams p = axis_params(c, ax);
+    PassParams p = rsfde_axis_params(c, ax);
     p.X = in;
     double* o = ax == 0 ? out : c->W[buf];
     p.Y = o;
@@ -589,7 +540,7 @@ static rsfde_status setup_fail(rsfde_ctx* c, rsfde_status st, const char* msg) {
   return st;
 }
 
-rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) {
+rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void* stream, bool alloc_work) {
   const auto t0 = std::chrono::steady_clock::now();
   if (!out) return RSFDE_E_CONFIG;
   *out = nullptr;
@@ -655,7 +606,7 @@ rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) 
   }
   // e-hat / e-check on the device
   {
-    ECoef e = ecoef_at(c, 0);
+    ECoef e = rsfde_ecoef_at(c, 0);
     if (c->ekind == RSFDE_COEF_GRID) e.grid = c->grid;
     double* part = nullptr;
     const int nblk = 148 * 4;
@@ -677,6 +628,11 @@ rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) 
     c->ebar = 0.5 * (mx + mn);
     if (!(mn > 0.0)) return setup_fail(c, RSFDE_E_COEFF, "e-check <= 0: e must be positive (P:33)");
   }
+  if (!alloc_work) {
+    c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = c;
+    return RSFDE_OK;
+  }
   // work memory
   const size_t vb = (size_t)G.NP * sizeof(double);
   double** bufs[] = {&c->W[0], &c->W[1], &c->W[2], &c->W[3], &c->Z, &c->X, &c->BUF, &c->U0, &c->FP, &c->FH, &c->TMP, &c->TMP2};
@@ -692,6 +648,10 @@ rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) 
   c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = c;
   return RSFDE_OK;
+}
+
+rsfde_status rsfde_setup(rsfde_ctx** out, const rsfde_problem* p, void* stream) {
+  return rsfde_setup_internal(out, p, stream, true);
 }
 
 rsfde_status rsfde_ebar(const rsfde_ctx* c, double* ebar, double* ehat, double* echeck) {

@@ -216,3 +216,126 @@ class RsfdeSolver:
             self.close()
         except Exception:
             pass
+
+
+class RsfdeTeam:
+    """Slab-sharded 3D solver (x_1 slabs over ``nranks`` ranks).
+
+    ``nlocal == nranks``: all ranks emulated in this process on the current device (vectors are the
+    whole dense grid).  ``nlocal == 1``: one rank per process (torch.distributed / torchrun); rank 0
+    creates the NCCL id (``nccl_unique_id``), the caller broadcasts it; vectors are the rank's slab
+    (``slab()`` gives its x_1 range)."""
+
+    def __init__(self, prob, nranks: int, rank: int = 0, nlocal: int = None, nccl_id: bytes = None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("rsfde needs a CUDA device (no CPU fallback)")
+        self.lib = L.load()
+        nlocal = nranks if nlocal is None else nlocal
+        self._solo = RsfdeSolver.__new__(RsfdeSolver)  # reuse the problem marshalling
+        a_half, b_half, gs, ks = prob.e_tables()
+        self._keep = [np.ascontiguousarray(a_half), np.ascontiguousarray(b_half)]
+        pr = L.rsfde_problem()
+        pr.d = prob.d
+        for i in range(3):
+            pr.n[i] = prob.n[i]
+            pr.alpha[i] = prob.alpha[i]
+            pr.kappa[i] = prob.kappa[i]
+        pr.tau_t = prob.tau
+        pr.M = prob.M
+        pr.e.kind = L.COEF_SEPARABLE
+        pr.e.a_half = _dp(self._keep[0])
+        pr.e.b_half = _dp(self._keep[1])
+        for i in range(3):
+            gi = None if gs[i] is None else np.ascontiguousarray(gs[i])
+            ki = None if ks[i] is None else np.ascontiguousarray(ks[i])
+            self._keep += [gi, ki]
+            pr.e.g[i] = _dp(gi)
+            pr.e.k[i] = _dp(ki)
+        self._prob_struct = pr
+        self.n = tuple(prob.n)
+        self.M = prob.M
+        self.nranks, self.rank, self.nlocal = nranks, rank, nlocal
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+        t = C.c_void_p()
+        st = self.lib.rsfde_team_setup(C.byref(t), C.byref(pr), nranks, rank, nlocal,
+                                       None if idbuf is None else C.cast(idbuf, C.c_void_p), _stream(stream))
+        if st != L.OK:
+            raise L.RsfdeError(st, self.lib.rsfde_team_last_error(None).decode())
+        self.team = t
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        lib = L.load()
+        buf = C.create_string_buffer(128)
+        st = lib.rsfde_nccl_unique_id(C.cast(buf, C.c_void_p))
+        if st != L.OK:
+            raise L.RsfdeError(st, lib.rsfde_team_last_error(None).decode())
+        return buf.raw
+
+    def _check(self, st):
+        if st != L.OK:
+            raise L.RsfdeError(st, self.lib.rsfde_team_last_error(self.team).decode())
+
+    def slab(self, local: int = 0):
+        lo, cnt = C.c_int(), C.c_int()
+        self._check(self.lib.rsfde_team_slab(self.team, local, C.byref(lo), C.byref(cnt)))
+        return lo.value, cnt.value
+
+    def local_shape(self):
+        if self.nlocal == self.nranks:
+            return self.n
+        return (self.slab(0)[1], self.n[1], self.n[2])
+
+    def empty(self):
+        import torch
+        return torch.empty(self.local_shape(), dtype=torch.float64, device="cuda")
+
+    def matvec(self, op: int, x, m: int = 0, out=None, stream=None):
+        y = self.empty() if out is None else out
+        self._check(self.lib.rsfde_team_matvec(self.team, op, m, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def precond(self, kind: int, x, out=None, stream=None):
+        y = self.empty() if out is None else out
+        self._check(self.lib.rsfde_team_precond_apply(self.team, kind, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def solve_steps(self, u, F=None, F_static=True, m_begin=0, m_count=None, cfg=None, stream=None):
+        m_count = self.M - m_begin if m_count is None else m_count
+        cfg = cfg or RsfdeSolver.cfg()
+        its = (C.c_int * max(1, m_count))()
+        rr = (C.c_double * max(1, m_count))()
+        cv = (C.c_ubyte * max(1, m_count))()
+        rep = L.rsfde_report()
+        rep.iters, rep.final_relres, rep.converged = its, rr, cv
+        self._check(self.lib.rsfde_team_solve_steps(self.team, m_begin, m_count, _ptr(u),
+                                                    None if F is None else _ptr(F), 1 if F_static else 0,
+                                                    C.byref(cfg), C.byref(rep), _stream(stream)))
+        return {"iters": list(its)[:m_count], "relres": list(rr)[:m_count],
+                "converged": [bool(v) for v in cv][:m_count], "loop_seconds": rep.loop_seconds,
+                "total_iters": rep.total_iters}
+
+    def compact_source(self, f_closed_slab, local: int = 0, out=None, stream=None):
+        """F on the local slab from f on the closed slab (count+2, n2+2, n3+2)."""
+        lo, cnt = self.slab(local)
+        y = out if out is not None else __import__("torch").empty((cnt, self.n[1], self.n[2]),
+                                                                   dtype=__import__("torch").float64, device="cuda")
+        self._check(self.lib.rsfde_team_compact_source(self.team, local, _ptr(f_closed_slab), _ptr(y), _stream(stream)))
+        return y
+
+    def launch_count(self, reset=False) -> int:
+        return int(self.lib.rsfde_team_launch_count(self.team, 1 if reset else 0))
+
+    def close(self):
+        if getattr(self, "team", None):
+            self.lib.rsfde_team_destroy(self.team)
+            self.team = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
