@@ -26,6 +26,31 @@ __global__ void __launch_bounds__(128) pattA(const double* __restrict__ x, doubl
   }
 }
 
+// A32: each warp owns 2 adjacent pairs (32 B = one sector per row); lane g loads/stores rows
+// g + 32 m with two adjacent 16-byte accesses (CTA = 4 warps = 128 B per row)
+__global__ void __launch_bounds__(128) pattA32(const double* __restrict__ x, double* __restrict__ y) {
+  const int g = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long off = 16LL * blockIdx.x + 4 * w;
+  double2 v[16], u[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int j = g + 32 * m;
+    if (j >= 1 && j <= N1) {
+      const double2* q = reinterpret_cast<const double2*>(x + off + (j - 1) * STRIDE);
+      v[m] = __ldg(q);
+      u[m] = __ldg(q + 1);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int j = g + 32 * m;
+    if (j >= 1 && j <= N1) {
+      double2* q = reinterpret_cast<double2*>(y + off + (j - 1) * STRIDE);
+      q[0] = v[m];
+      q[1] = u[m];
+    }
+  }
+}
 // E: per-lane row loads (as A), stores staged through smem and written coalesced (64 B/row)
 __global__ void __launch_bounds__(128) pattE(const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ double2 tile_raw[];
@@ -101,6 +126,8 @@ int main() {
   for (int it = 0; it < 2; ++it) {
     cudaEventRecord(a); pattA<<<pairs / 4, 128>>>(x, y); cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b); printf("A  lane-per-row, 64 B/CTA/row        %.3f ms  %.0f GB/s\n", ms, bytes / ms / 1e6);
+    cudaEventRecord(a); pattA32<<<pairs / 8, 128>>>(x, y); cudaEventRecord(b); cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b); printf("A32 lane-per-row, 32 B/warp, 128 B/CTA %.3f ms  %.0f GB/s\n", ms, bytes / ms / 1e6);
     cudaEventRecord(a); pattE<<<pairs / 4, 128, 512 * 4 * 16>>>(x, y); cudaEventRecord(b); cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b); printf("E  row-per-lane loads, coalesced stores %.3f ms  %.0f GB/s\n", ms, bytes / ms / 1e6);
     cudaEventRecord(a); pattF<<<pairs / 4, 128, 512 * 4 * 16>>>(x, y); cudaEventRecord(b); cudaEventSynchronize(b);
