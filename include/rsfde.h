@@ -96,14 +96,18 @@ enum {
 };
 
 enum { RSFDE_X0_PREV = 0, RSFDE_X0_ZERO = 1 };
-enum { RSFDE_FORM_A = 0, RSFDE_FORM_ATILDE = 1 };
+/* FORM_A: P_hat^{-1} A u = P_hat^{-1} b (== the paper's one-sided system, default);
+   FORM_ATILDE: the literal P_alpha^{-1} A~ u = P_alpha^{-1} b~ chain;
+   FORM_TWO_SIDED: the two-sided system P_alpha^{-1/2} A~ P_alpha^{-1/2} u~ = P_alpha^{-1/2} b~,
+   u = P_alpha^{-1/2} u~ (Eq.(Pls)), started from u~_0 = P_alpha^{1/2} x_0 (Thm 3.9). */
+enum { RSFDE_FORM_A = 0, RSFDE_FORM_ATILDE = 1, RSFDE_FORM_TWO_SIDED = 2 };
 
 typedef struct {
   int restart;      /* GMRES(m) restart length, 1..50 */
   int max_iters;    /* cap on Arnoldi steps per solve (<= 0: 10*restart) */
   double tol;       /* stop when |g_{j+1}| <= tol * ||r_0|| (preconditioned residual) */
   int x0_policy;    /* RSFDE_X0_PREV: x_0 = u^{(m)} (default); RSFDE_X0_ZERO */
-  int form;         /* RSFDE_FORM_A (default) or RSFDE_FORM_ATILDE (literal A~ / P_alpha chain) */
+  int form;         /* RSFDE_FORM_A (default), RSFDE_FORM_ATILDE or RSFDE_FORM_TWO_SIDED */
   int fixed_iters;  /* > 0: run exactly this many Arnoldi steps (replay mode for parity) */
 } rsfde_gmres_cfg;
 

@@ -26,6 +26,7 @@ class GmresResult:
     converged: bool
     relres_est: float              # |g_{k+1}| / beta0 (Givens estimate)
     history: List[float] = field(default_factory=list)
+    beta0: float = 0.0             # ||r_0|| of the first cycle (history * beta0 = ||r_j||)
 
 
 def _dot(a, b):
@@ -42,7 +43,7 @@ def gmres(apply_K: Callable[[np.ndarray], np.ndarray], c: np.ndarray, x0: np.nda
     beta0 = math.sqrt(_dot(r, r))
     hist = [1.0]
     if beta0 == 0.0 or (fixed_iters is not None and fixed_iters <= 0):
-        return GmresResult(x, 0, True, 0.0, hist)
+        return GmresResult(x, 0, True, 0.0, hist, beta0)
     total = 0
     while True:
         beta = math.sqrt(_dot(r, r))
@@ -96,5 +97,5 @@ def gmres(apply_K: Callable[[np.ndarray], np.ndarray], c: np.ndarray, x0: np.nda
         if breakdown:
             converged = True
         if converged or total >= max_iters:
-            return GmresResult(x, total, converged, abs(g[k]) / beta0, hist)
+            return GmresResult(x, total, converged, abs(g[k]) / beta0, hist, beta0)
         r = c - apply_K(x)                              # explicit residual, restart

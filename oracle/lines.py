@@ -114,6 +114,10 @@ class LineSystem:
     def P_alpha_inv_sqrt(self, ebar, U):
         return self.dst(self.dst(U) / np.sqrt(self.lambda_P(ebar)))
 
+    def P_alpha_sqrt(self, ebar, U):
+        """P_alpha^{1/2} U = S Lambda_P^{1/2} S U (maps u to the two-sided unknown u~)."""
+        return self.dst(self.dst(U) * np.sqrt(self.lambda_P(ebar)))
+
     def P_hat_inv(self, ebar, U):
         """(H_alpha P_alpha)^{-1} U = S (Lambda_P Lambda_H)^{-1} S U (SURVEY 8 key identity)."""
         return self.dst(self.dst(U) / (self.lambda_P(ebar) * self.lambda_H()))

@@ -122,9 +122,12 @@ def solve(prob, steps: Optional[int] = None, u0: Optional[np.ndarray] = None,
           fixed_iters: Optional[List[int]] = None, restart: Optional[int] = None,
           tol: Optional[float] = None, max_iters: Optional[int] = None,
           ebar: Optional[float] = None, F_static: Optional[np.ndarray] = None,
-          tier: str = "L"):
-    """March ``steps`` CN steps (default M) of Eq.(tls) with one-sided tau-preconditioned GMRES.
+          tier: str = "L", sided: int = 1):
+    """March ``steps`` CN steps (default M) of Eq.(tls) with tau-preconditioned GMRES.
 
+    sided=1: the one-sided system P^{-1} A~ u = P^{-1} b~ (Eq.(one-sided), P:217-221);
+    sided=2: the two-sided system P^{-1/2} A~ P^{-1/2} u~ = P^{-1/2} b~, u = P^{-1/2} u~ (Eq.(Pls),
+    P:223-232), started from u~_0 = P^{1/2} u^{(m)} (so that u_0 = u^{(m)}, Thm 3.9).
     Returns (u, report, ebar).  ``tier='D'`` uses dense matrices (tiny grids)."""
     steps = prob.M if steps is None else steps
     restart = prob.restart if restart is None else restart
@@ -138,25 +141,37 @@ def solve(prob, steps: Optional[int] = None, u0: Optional[np.ndarray] = None,
         Ds = D.DenseSystem(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau)
         Pinv = np.linalg.inv(Ds.P_alpha(ebar))
         Hinv = np.linalg.inv(Ds.H_alpha())
+        w, Q = np.linalg.eigh(Ds.P_alpha(ebar))
+        Pmh = (Q / np.sqrt(w)) @ Q.T       # P^{-1/2}
+        Pph = (Q * np.sqrt(w)) @ Q.T       # P^{1/2}
     else:
         Ls = LineSystem(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau)
     for m in range(steps):
         e = prob.e_grid(prob.t_half(m))
         F = F_static if F_static is not None else source_F(prob, m)
+        fx = None if fixed_iters is None else fixed_iters[m]
         if tier == "D":
-            Kmat = Pinv @ Ds.A_tilde(e)
             b = Ds.b(e, D.vec(u), D.vec(F))
-            c = Pinv @ (Hinv @ b)
-            res = gmres(lambda v: Kmat @ v, c, D.vec(u), restart, tol, max_iters,
-                        None if fixed_iters is None else fixed_iters[m])
-            u_new = D.unvec(res.x, prob.n)
+            if sided == 1:
+                Kmat = Pinv @ Ds.A_tilde(e)
+                res = gmres(lambda v: Kmat @ v, Pinv @ (Hinv @ b), D.vec(u), restart, tol, max_iters, fx)
+                u_new = D.unvec(res.x, prob.n)
+            else:
+                Kmat = Pmh @ Ds.A_tilde(e) @ Pmh
+                res = gmres(lambda v: Kmat @ v, Pmh @ (Hinv @ b), Pph @ D.vec(u), restart, tol, max_iters, fx)
+                u_new = D.unvec(Pmh @ res.x, prob.n)
         else:
             b = Ls.rhs(e, u, F)
-            c = Ls.P_alpha_inv(ebar, Ls.H_alpha_inv(b))
-            K = lambda v: Ls.P_alpha_inv(ebar, Ls.A_tilde(e, v))
-            res = gmres(K, c, u, restart, tol, max_iters,
-                        None if fixed_iters is None else fixed_iters[m])
-            u_new = res.x
+            if sided == 1:
+                c = Ls.P_alpha_inv(ebar, Ls.H_alpha_inv(b))
+                K = lambda v: Ls.P_alpha_inv(ebar, Ls.A_tilde(e, v))
+                res = gmres(K, c, u, restart, tol, max_iters, fx)
+                u_new = res.x
+            else:
+                c = Ls.P_alpha_inv_sqrt(ebar, Ls.H_alpha_inv(b))
+                K = lambda v: Ls.P_alpha_inv_sqrt(ebar, Ls.A_tilde(e, Ls.P_alpha_inv_sqrt(ebar, v)))
+                res = gmres(K, c, Ls.P_alpha_sqrt(ebar, u), restart, tol, max_iters, fx)
+                u_new = Ls.P_alpha_inv_sqrt(ebar, res.x)
         rep.iters.append(res.iters)
         rep.relres.append(res.relres_est)
         rep.converged.append(res.converged)

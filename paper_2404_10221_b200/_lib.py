@@ -18,7 +18,7 @@ COEF_SEPARABLE, COEF_GRID = 0, 1
 OP_A, OP_ATILDE, OP_S_ALPHA, OP_H_ALPHA, OP_H_ALPHA_INV, OP_K = range(6)
 PHAT_INV, PALPHA_INV, PALPHA_INV_SQRT = range(3)
 X0_PREV, X0_ZERO = 0, 1
-FORM_A, FORM_ATILDE = 0, 1
+FORM_A, FORM_ATILDE, FORM_TWO_SIDED = 0, 1, 2
 STATUS_NAMES = {0: "RSFDE_OK", 1: "RSFDE_E_DIM", 2: "RSFDE_E_DOMAIN", 3: "RSFDE_E_COEFF",
                 4: "RSFDE_E_CONFIG", 5: "RSFDE_E_CUDA", 6: "RSFDE_E_NCCL", 7: "RSFDE_E_NOMEM"}
 

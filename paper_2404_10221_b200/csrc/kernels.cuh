@@ -23,7 +23,12 @@ struct ECoef {
   const double* grid;        // kind 2: dense layout [x1][x2][x3], N values
 };
 
-enum SpecKind { SPEC_PHAT = 0, SPEC_PALPHA = 1, SPEC_PALPHA_SQRT = 2, SPEC_HINV = 3 };
+// the last-axis pass divides by Lambda(k):
+//   PHAT: Lambda_P Lambda_H      PALPHA: Lambda_P        PALPHA_SQRT: Lambda_P^{1/2}
+//   HINV: Lambda_H               PALPHA_RSQRT: Lambda_P^{-1/2} (i.e. multiplies by Lambda_P^{1/2})
+//   HP_SQRT: Lambda_H Lambda_P^{1/2} (P_alpha^{-1/2} H^{-1}, the two-sided left factor)
+enum SpecKind { SPEC_PHAT = 0, SPEC_PALPHA = 1, SPEC_PALPHA_SQRT = 2, SPEC_HINV = 3, SPEC_PALPHA_RSQRT = 4,
+                SPEC_HP_SQRT = 5 };
 
 // spectrum tables for the preconditioner scaling on the last axis
 struct Spec {

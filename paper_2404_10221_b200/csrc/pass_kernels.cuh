@@ -203,6 +203,8 @@ __device__ __forceinline__ double2 spec_pair(const PassParams& p, const PencilCo
     case SPEC_PHAT: return make_double2(lPp * (kc.cH_p * lh), lPq * (kc.cH_q * lh));
     case SPEC_PALPHA: return make_double2(lPp, lPq);
     case SPEC_PALPHA_SQRT: return make_double2(sqrt(lPp), sqrt(lPq));
+    case SPEC_PALPHA_RSQRT: return make_double2(1.0 / sqrt(lPp), 1.0 / sqrt(lPq));
+    case SPEC_HP_SQRT: return make_double2(kc.cH_p * lh * sqrt(lPp), kc.cH_q * lh * sqrt(lPq));
     default: return make_double2(kc.cH_p * lh, kc.cH_q * lh);
   }
 }
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
   const int grp = threadIdx.x / G;
   const int g = threadIdx.x % G;
   double2* buf = smem + grp * L;
-  const double rs = (OPER && p.rscale) ? __ldg(p.rscale) : 1.0;
+  const double rs = p.rscale ? __ldg(p.rscale) : 1.0;  // lazy basis normalisation of the input
   const double hs = 0.5 * p.dst_scale;
   {
     const long long pair = (long long)blockIdx.x * GROUPS + grp;
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
       }
     } else {
 #pragma unroll
-      for (int m = 0; m < E / 2; ++m) v[m] = ld_pair(p, p.X, pc, g + G * m);
+      for (int m = 0; m < E / 2; ++m) v[m] = c_scale(ld_pair(p, p.X, pc, g + G * m), rs);
       odd_extend<T>(v, buf, g);
     }
 

@@ -308,7 +308,8 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
 }
 
 // y = S Lambda^{-1} S x for the spectrum kind (DSTs along every axis, scaling on the last)
-static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, double* out, cudaStream_t s) {
+static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, double* out, cudaStream_t s,
+                                  const double* xscale = nullptr) {
   const int d = c->d;
   const double* in = x;
   int buf = 0;
@@ -317,6 +318,7 @@ static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, doubl
     const bool last = ax == d - 1;
     p.X = in;
     p.spec.kind = kind;
+    if (ax == 0) p.rscale = xscale;
     double* o = (last && d == 1) ? out : c->W[buf];
     p.Y = o;
     LAUNCH(PC_DST, 16.0 * (double)c->geo.NP, launch_dst_pass(p, last, s), "dst pass");
@@ -370,6 +372,14 @@ static rsfde_status apply_K(rsfde_ctx* c, int form, int m, const double* v, cons
     a.spec = SPEC_PHAT;
     return oper_chain(c, a, z, s);
   }
+  if (form == RSFDE_FORM_TWO_SIDED) {
+    // P_alpha^{-1/2} H^{-1} A P_alpha^{-1/2} v  (Eq.(Pls): A~ = H^{-1} A)
+    TRY(precond_chain(c, SPEC_PALPHA_SQRT, v, c->TMP2, s, vscale));
+    a.R = c->TMP2;
+    a.rscale = nullptr;
+    TRY(oper_chain(c, a, c->TMP, s));
+    return precond_chain(c, SPEC_HP_SQRT, c->TMP, z, s);
+  }
   TRY(oper_chain(c, a, c->TMP, s));
   TRY(precond_chain(c, SPEC_HINV, c->TMP, c->TMP2, s));
   return precond_chain(c, SPEC_PALPHA, c->TMP2, z, s);
@@ -387,6 +397,7 @@ static rsfde_status precond_residual(rsfde_ctx* c, int form, int m, const double
   a.bcoef = 1.0;
   TRY(oper_chain(c, a, c->TMP, s));
   if (form == RSFDE_FORM_A) return precond_chain(c, SPEC_PHAT, c->TMP, out, s);
+  if (form == RSFDE_FORM_TWO_SIDED) return precond_chain(c, SPEC_HP_SQRT, c->TMP, out, s);
   TRY(precond_chain(c, SPEC_HINV, c->TMP, c->TMP2, s));
   return precond_chain(c, SPEC_PALPHA, c->TMP2, out, s);
 }
@@ -423,7 +434,22 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
   Flags fl{0, 0, 1.0};
   bool converged = false;
   while (true) {
-    if (first && mode_fast && form == RSFDE_FORM_A) {
+    if (form == RSFDE_FORM_TWO_SIDED) {
+      // residual of the physical iterate u = P^{-1/2} u~ (X holds u on the first cycle, u~ later)
+      if (!have_b) {
+        TRY(compute_b(c, m, s));
+        have_b = true;
+      }
+      if (first) {
+        TRY(precond_residual(c, form, m, c->BUF, c->X, c->V[0], s));
+        // X <- u~_0 = P^{1/2} u_0 (Thm 3.9)
+        TRY(precond_chain(c, SPEC_PALPHA_RSQRT, c->X, c->Z, s));
+        CK(cudaMemcpyAsync(c->X, c->Z, (size_t)NP * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
+      } else {
+        TRY(precond_chain(c, SPEC_PALPHA_SQRT, c->X, c->Z, s));
+        TRY(precond_residual(c, form, m, c->BUF, c->Z, c->V[0], s));
+      }
+    } else if (first && mode_fast && form == RSFDE_FORM_A) {
       ChainArgs a;
       a.xmode = X_INPUT;
       a.Xin = c->FH;
@@ -476,6 +502,10 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
     converged = fixed > 0 ? true : (fl.converged != 0 || fl.breakdown != 0);
     if (converged || total >= max_iters) break;
     first = false;
+  }
+  if (form == RSFDE_FORM_TWO_SIDED) {  // u = P^{-1/2} u~
+    TRY(precond_chain(c, SPEC_PALPHA_SQRT, c->X, c->Z, s));
+    CK(cudaMemcpyAsync(c->X, c->Z, (size_t)NP * sizeof(double), cudaMemcpyDeviceToDevice, s), "copy");
   }
   if (iters_out) *iters_out = total;
   if (relres_out) *relres_out = fl.relres;
@@ -740,7 +770,7 @@ rsfde_status rsfde_compact_source(rsfde_ctx* c, const double* f_closed, double* 
 
 static rsfde_status check_cfg(rsfde_ctx* c, const rsfde_gmres_cfg* cfg) {
   if (!cfg || cfg->restart < 1 || cfg->restart > 50 || (cfg->fixed_iters <= 0 && !(cfg->tol >= 0.0)) ||
-      (cfg->form != RSFDE_FORM_A && cfg->form != RSFDE_FORM_ATILDE) ||
+      (cfg->form != RSFDE_FORM_A && cfg->form != RSFDE_FORM_ATILDE && cfg->form != RSFDE_FORM_TWO_SIDED) ||
       (cfg->x0_policy != RSFDE_X0_PREV && cfg->x0_policy != RSFDE_X0_ZERO)) {
     c->err = "bad GMRES configuration (restart in 1..50, tol >= 0, form, x0_policy)";
     return RSFDE_E_CONFIG;
@@ -830,7 +860,7 @@ rsfde_status rsfde_solve_steps(rsfde_ctx* c, int m_begin, int m_count, double* u
       CK(cudaMemsetAsync(c->X, 0, vb, s), "memset x");
       TRY(gmres_core(c, m, false, true, *cfg, s, &its, &rr, &conv));
     } else {
-      TRY(gmres_core(c, m, true, false, *cfg, s, &its, &rr, &conv));
+      TRY(gmres_core(c, m, cfg->form != RSFDE_FORM_TWO_SIDED, false, *cfg, s, &its, &rr, &conv));
     }
     total += its;
     if (rep) {

@@ -249,3 +249,44 @@ def test_invalid_arguments_fail_loudly():
     with pytest.raises(L.RsfdeError) as ei:
         RsfdeSolver.from_problem(p)
     assert ei.value.status == L.E_DOMAIN
+
+
+# ----------------------------------------------------------------------- two-sided system (NEXT-1)
+@pytest.mark.parametrize("name", ["c1", "c5s", "ex2"])
+def test_two_sided_march_parity(name):
+    from paper_2404_10221_b200 import _lib as L
+    prob = {"c1": lambda: I.config_c1(n=127, M=8),
+            "c5s": lambda: I.config_c5(M=3, nn=(31, 15, 63)),
+            "ex2": lambda: I.example(2, 31, 8, (1.5, 1.7))}[name]()
+    u, rep = _march(prob, form=L.FORM_TWO_SIDED)
+    Fst = scheme.source_F(prob, 0) if prob.source_static else None
+    uo, ro, _ = scheme.solve(prob, F_static=Fst, sided=2)
+    assert all(rep["converged"])
+    assert max(abs(a - b) for a, b in zip(rep["iters"], ro.iters)) <= 1, (rep["iters"], ro.iters)
+    if rep["iters"] != ro.iters:
+        uo, ro, _ = scheme.solve(prob, F_static=Fst, sided=2, fixed_iters=rep["iters"])
+    assert relerr(u, uo) < 1e-9
+    # one- and two-sided solve the same linear systems
+    u1, _ = _march(prob)
+    assert relerr(u, u1) < 10 * prob.tol
+
+
+def test_two_sided_gmres_step():
+    from paper_2404_10221_b200 import _lib as L
+    from paper_2404_10221_b200.solver import RsfdeSolver
+    prob = I.config_c5(M=2, nn=(15, 7, 31))
+    S = RsfdeSolver.from_problem(prob)
+    Ls = LineSystem(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau)
+    ebar = scheme.e_bar(prob)[0]
+    e = prob.e_grid(prob.t_half(1))
+    b = I.seeded_vector(8, prob.n)
+    x0 = 0.2 * I.seeded_vector(9, prob.n)
+    K = lambda v: Ls.P_alpha_inv_sqrt(ebar, Ls.A_tilde(e, Ls.P_alpha_inv_sqrt(ebar, v)))
+    c = Ls.P_alpha_inv_sqrt(ebar, Ls.H_alpha_inv(b))
+    ref = oracle_gmres(K, c, Ls.P_alpha_sqrt(ebar, x0), 20, 1e-11, 200)
+    xd = _dev(x0)
+    its, rr, conv = S.gmres_step(1, _dev(b), xd, S.cfg(restart=20, tol=1e-11, form=L.FORM_TWO_SIDED))
+    assert conv and abs(its - ref.iters) <= 1
+    if its != ref.iters:
+        ref = oracle_gmres(K, c, Ls.P_alpha_sqrt(ebar, x0), 20, 1e-11, 200, fixed_iters=its)
+    assert relerr(_host(xd), Ls.P_alpha_inv_sqrt(ebar, ref.x)) < 1e-9

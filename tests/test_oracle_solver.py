@@ -133,3 +133,43 @@ def test_crank_nicolson_second_order_in_time():
         errs.append(np.abs(u - p.exact(p.mesh(), 1.0)).max())
     r = [errs[0] / errs[1], errs[1] / errs[2]]
     assert all(3.6 < x < 4.4 for x in r), r
+
+
+# ---------------------------------------------------------------- two-sided system (NEXT-1)
+@pytest.mark.parametrize("shape", [(9,), (5, 4), (4, 3, 5)])
+def test_two_sided_equals_direct_solution(shape):
+    # Eq.(Pls): u = P^{-1/2} u~ solves Eq.(tls); tier D and tier L agree
+    d = len(shape)
+    p = I.config_c5(M=3, nn=shape) if d == 3 else I.config_c1(n=shape[0], M=3)
+    if d == 2:
+        p = I.config_c2(n=5, M=3)
+        p.n = shape
+        p.source = lambda xs, t: np.cos(xs[0] + 2 * xs[1] + t)
+    u2, rep2, _ = scheme.solve(p, tol=1e-13, tier="D", sided=2)
+    Ds = D.DenseSystem(p.d, p.n, p.alpha, p.kappa, p.tau)
+    v = D.vec(p.psi_interior())
+    for m in range(p.M):
+        e = p.e_grid(p.t_half(m))
+        v = np.linalg.solve(Ds.A(e), Ds.b(e, v, D.vec(scheme.source_F(p, m))))
+    assert np.max(np.abs(D.vec(u2) - v)) < 1e-10 * max(1e-30, np.abs(v).max())
+    uL, repL, _ = scheme.solve(p, tol=1e-13, tier="L", sided=2)
+    assert repL.iters == rep2.iters
+    assert np.max(np.abs(uL - u2)) < 1e-12 * np.abs(u2).max()
+
+
+def test_theorem_3_9_one_vs_two_sided_residuals():
+    # Theorem 3.9: with u_0 = P^{-1/2} u~_0, ||r_j||_2 <= ||r~_j||_2 / sqrt(ebar) at every j
+    from oracle.lines import LineSystem
+    p = I.config_c5(M=2, nn=(7, 6, 9))
+    Ls = LineSystem(p.d, p.n, p.alpha, p.kappa, p.tau)
+    ebar = scheme.e_bar(p)[0]
+    e = p.e_grid(p.t_half(0))
+    b = Ls.rhs(e, np.zeros(p.n), scheme.source_F(p, 0))
+    u0 = 0.3 * I.seeded_vector(3, p.n)
+    K1 = lambda v: Ls.P_alpha_inv(ebar, Ls.A_tilde(e, v))
+    K2 = lambda v: Ls.P_alpha_inv_sqrt(ebar, Ls.A_tilde(e, Ls.P_alpha_inv_sqrt(ebar, v)))
+    r1 = gmres(K1, Ls.P_alpha_inv(ebar, Ls.H_alpha_inv(b)), u0, 50, 0.0, 12, fixed_iters=12)
+    r2 = gmres(K2, Ls.P_alpha_inv_sqrt(ebar, Ls.H_alpha_inv(b)), Ls.P_alpha_sqrt(ebar, u0), 50, 0.0, 12,
+               fixed_iters=12)
+    for j in range(13):
+        assert r1.history[j] * r1.beta0 <= r2.history[j] * r2.beta0 / math.sqrt(ebar) * (1 + 1e-10)
