@@ -1,0 +1,431 @@
+// Warp-specialised tile pipeline for the L = 1024 pencil passes (n = 511: the C5 hot path).
+//
+// A CTA (one per SM, persistent) = 8 compute warps + 1 producer warp.  A tile = 8 adjacent pencil
+// pairs: on a strided axis 16 adjacent pencils = 128 contiguous bytes of every row, on the
+// contiguous axis 16 adjacent rows.  The producer streams each tile input into one shared stage with
+// cp.async.bulk (one 128-byte row piece or one 4 KB row per copy) tracked by an mbarrier
+// transaction count; the compute warps read their pair's column out of the stage, release it (so
+// the next input streams in while they compute) and run the FFT phases of pass_kernels.cuh with the
+// same per-pair shared buffers.  Strided outputs go out as 128-byte rows stored cooperatively by
+// the 8 compute warps (measured: 128-byte row tiles move 2.9x faster than one row per lane,
+// tools/micro/pattern_micro.cu).  Neighbouring pairs are processed in lockstep, so every DRAM
+// sector is read and written once (ncu).
+//
+// Job sequence per tile (consumed in the same order by producer and compute warps):
+//   spectral operator pass:  [R_t] [X_t (X_INPUT) | R_t again (X = E o R)]      (X_ZERO: [R_t])
+//   DST pass:                [X_t]
+#pragma once
+#include "pass_kernels.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+
+namespace rsfde {
+
+// experiments only (tools/tile_variants.sh): bit 1 = skip the FFTs, bit 2 = skip the global stores
+#ifndef RSFDE_TILE_SKIP
+#define RSFDE_TILE_SKIP 0
+#endif
+
+constexpr int kTilePairs = 4;                        // pencil pairs per tile (one compute warp each)
+constexpr int kTilePencils = 2 * kTilePairs;          // adjacent pencils per tile
+constexpr int kRowBytes = 8 * kTilePencils;           // bytes of one tile row on a strided axis
+// 3 warpgroups: warpgroups 0-1 = the 8 compute warps, warpgroup 2 = the producer warp (+3 idle
+// warps).  The producer warpgroup gives its registers to the compute warps (setmaxnreg): launched at
+// 168 registers/thread, compute warps run at 232 (no spills), the producer at 40.
+constexpr int kTileThreads = kTilePairs == 8 ? 384 : 256;
+constexpr int kCtasPerSm = kTilePairs == 8 ? 1 : 2;
+constexpr int kProducerRegs = 40;
+constexpr int kComputeRegs = kTilePairs == 8 ? 232 : 216;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kTilePairs) : "memory"); }
+
+// element offset of the first pencil of tile t (strided: pencil 16t; contiguous: row 16t)
+__device__ __forceinline__ long long tile_base(const PassParams& p, long long t) {
+  if (p.contiguous) return kTilePencils * t * p.geo.P;
+  const long long pen = kTilePencils * t;
+  const long long o = pen / p.inner, i = pen % p.inner;
+  return o * (long long)p.n * p.inner + i;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Stage layout.  Strided axis: tensor map {inner, n, outer} (pencil, axis position, outer block),
+// box {16, 256, 1} with the 128-byte swizzle -> stage row r (axis position r + 1) holds the 16
+// pencils of the tile as 8 chunks of 16 bytes (one per pair), chunk w stored at w ^ (r & 7).
+// Contiguous axis: tensor map {P, rows}, box {256, 16} -> stage[half][row][256].
+constexpr int kBoxRows = 256;
+constexpr size_t kStageBytes = 2 * kBoxRows * kRowBytes;  // both layouts, n <= 511
+
+// producer: one lane streams one tile input into the stage (two box copies)
+__device__ __forceinline__ void produce(const PassParams& p, const CUtensorMap* tm, long long t, char* stage,
+                                        unsigned long long* full) {
+  mbar_expect_tx(full, (unsigned)kStageBytes);
+  if (p.contiguous) {
+    tma_load_3d(stage, tm, 0, (int)(kTilePencils * t), 0, full);
+    tma_load_3d(stage + kStageBytes / 2, tm, kBoxRows, (int)(kTilePencils * t), 0, full);
+  } else {
+    const long long pen = kTilePencils * t;
+    const int o = (int)(pen / p.inner), i = (int)(pen % p.inner);
+    tma_load_3d(stage, tm, i, 0, o, full);
+    tma_load_3d(stage + kStageBytes / 2, tm, i, kBoxRows, o, full);
+  }
+}
+
+// value pair (p, q) of compute warp w at axis position j (1..n) from the stage
+__device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* stage, int w, int j) {
+  const int r = j - 1;
+  if (p.contiguous) {
+    const double* s = reinterpret_cast<const double*>(stage) + (r >> 8) * (kTilePencils * kBoxRows) + (r & 255);
+    return make_double2(s[(2 * w) * kBoxRows], s[(2 * w + 1) * kBoxRows]);
+  }
+  // 128-byte swizzle: 16-byte chunk c of row r at c ^ (r & 7); 64-byte swizzle: c ^ ((r >> 1) & 3)
+  const int sw = kTilePairs == 8 ? (r & 7) : ((r >> 1) & 3);
+  return *reinterpret_cast<const double2*>(stage + (size_t)r * kRowBytes + ((w ^ sw) << 4));
+}
+
+// XOR swizzle of the per-pair output buffers so that the cooperative row stores read
+// conflict-free across the 8 buffers
+__device__ __forceinline__ int oswz(int k, int w) { return k ^ (w & 7); }
+
+template <int MODE>
+__global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR,
+                                                          const __grid_constant__ CUtensorMap tmX) {
+  using T = Lay2<32, 32>;
+  constexpr int E = 32, G = 32, L = 1024, N = 512;
+  constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
+  constexpr bool LAST = MODE == MODE_OPER_SPEC_LAST || MODE == MODE_DST_LAST;
+  extern __shared__ __align__(128) char tsm_raw[];
+  char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);  // TMA swizzle needs 1 KB alignment
+  double2* bufs = reinterpret_cast<double2*>(tsm);                        // 8 x 16 KB
+  char* stage = tsm + (size_t)kTilePairs * L * sizeof(double2);           // 1024-aligned
+  __shared__ __align__(8) unsigned long long full_bar, empty_bar;
+  __shared__ int tvalid[kTilePairs];  // validity bits (p, q) of each warp's pair in the current tile
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long ntiles = p.contiguous ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
+  const int jobs_per_tile = OPER ? (p.xmode == X_ZERO ? 1 : 2) : 1;
+  if (threadIdx.x == 0) {
+    mbar_init(&full_bar, 1);
+    mbar_init(&empty_bar, kTilePairs);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp >= kTilePairs) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+    if (warp != kTilePairs) return;
+    // ------------------------------------------------------------------ producer warp
+    long long job = 0;
+    for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int k = 0; k < jobs_per_tile; ++k, ++job) {
+        if (job > 0) mbar_wait(&empty_bar, (unsigned)((job - 1) & 1));
+        const CUtensorMap* src = OPER ? ((k == 0 || p.xmode == X_E_TIMES_R) ? &tmR : &tmX) : &tmX;
+        if (lane == 0) produce(p, src, t, stage, &full_bar);
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- compute warps
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kComputeRegs));
+  const int w = warp, g = lane;
+  double2* buf = bufs + w * L;
+  const double rs = p.rscale ? __ldg(p.rscale) : 1.0;
+  const double hs = 0.5 * p.dst_scale;
+  long long job = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long pair = (long long)kTilePairs * t + w;
+    const bool active = pair < p.npairs;
+    const PairCtx pc = make_pair(p, active ? pair : 0, active);
+    if (lane == 0) tvalid[w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
+    double2 v[E];
+    // ---- job 0: primary input
+    mbar_wait(&full_bar, (unsigned)(job & 1));
+    if (OPER) {
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const int j = g + G * m;
+        double2 r = make_double2(0.0, 0.0);
+        if (m < E / 2 && j >= 1 && j <= p.n) {
+          r = stage_pair(p, stage, w, j);
+          r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
+        }
+        v[m] = r;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < E / 2; ++m) {
+        const int j = g + G * m;
+        double2 r = make_double2(0.0, 0.0);
+        if (j >= 1 && j <= p.n) {
+          r = stage_pair(p, stage, w, j);
+          r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
+        }
+        v[m] = r;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar);
+    ++job;
+    if (!OPER) odd_extend<T>(v, buf, g);
+
+    const int first = OPER ? 0 : 2;
+    const int last_phase = LAST ? 3 : 2;
+#pragma unroll 1
+    for (int ph = first; ph <= last_phase; ++ph) {
+      if (!(RSFDE_TILE_SKIP & 1)) T::fft(v, buf, g, p.tw, ph == 1);
+      if (ph == 0) {
+        // C = S H R = s lambda^H D(R) (non-last spectral pass), via the partner spectrum
+        if (!LAST) {
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < E; ++r) buf[T::rowk(g, r)] = v[r];
+          __syncwarp();
+          double2 cv[E / 2];
+#pragma unroll
+          for (int r = 0, i = 0; r < E; ++r) {
+            if (!T::lower(r)) continue;
+            const int k = T::rowk(g, r);
+            const double2 zm = buf[(L - k) & (L - 1)];
+            const double f = (k >= 1) ? hs * __ldg(p.lamH + k - 1) : 0.0;
+            cv[i++] = make_double2(-(v[r].y - zm.y) * f, (v[r].x - zm.x) * f);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int r = 0, i = 0; r < E; ++r) {
+            if (!T::lower(r)) continue;
+            buf[oswz(T::rowk(g, r), w)] = cv[i++];
+          }
+          // store C
+          if (p.contiguous) {
+            __syncwarp();
+            for (int j = g + 1; j <= p.n; j += 32) {
+              const double2 c = buf[oswz(j, w)];
+              if (RSFDE_TILE_SKIP & 2) continue;
+              if (pc.vp) p.C[pc.off_p + j - 1] = c.x;
+              if (pc.vq) p.C[pc.off_q + j - 1] = c.y;
+            }
+            __syncwarp();
+          } else {
+            compute_bar();
+            const long long base = tile_base(p, t);
+            for (int e = threadIdx.x; e < p.n * kTilePairs; e += 32 * kTilePairs) {
+              const int row = e / kTilePairs, q = e % kTilePairs;
+              const double2 c = bufs[q * L + oswz(row + 1, q)];
+              const int vm = tvalid[q];
+              if (!(vm & 1)) continue;
+              double* dst = p.C + base + (long long)row * p.stride + 2 * q;
+              if (RSFDE_TILE_SKIP & 2) continue;
+              if (vm & 2) *reinterpret_cast<double2*>(dst) = c;
+              else *dst = c.x;
+            }
+            compute_bar();
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
+      } else if (ph == 1) {
+        // X channel from the stage (job 1) into the pair buffer (x = X, or e o R), then
+        // y = H X + eta T R on j = g + G m with the stencil neighbours from the buffer
+        const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
+        if (p.xmode != X_ZERO) mbar_wait(&full_bar, (unsigned)(job & 1));
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m) {
+          const int j = g + G * m;
+          double2 x = make_double2(0.0, 0.0);
+          if (p.xmode != X_ZERO && j >= 1 && j <= p.n) {
+            x = stage_pair(p, stage, w, j);
+            if (p.xmode == X_E_TIMES_R) {
+              const double2 e = e_pair(p, pc, kc, j);
+              x = make_double2(rs * x.x * e.x, rs * x.y * e.y);
+            }
+            if (!pc.vp) x.x = 0.0;
+            if (!pc.vq) x.y = 0.0;
+          }
+          buf[j] = x;
+        }
+        if (g == 0) buf[N] = make_double2(0.0, 0.0);
+        if (p.xmode != X_ZERO) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar);
+          ++job;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E / 2; ++m) {
+          const int j = g + G * m;
+          double2 y = make_double2(0.0, 0.0);
+          if (j >= 1 && j <= p.n) {
+            const double2 xl = buf[j - 1], x0 = buf[j], xn = buf[j + 1];
+            y.x = fma(p.hc0, x0.x, fma(p.hc1, xl.x + xn.x, p.eta * v[m].x));
+            y.y = fma(p.hc0, x0.y, fma(p.hc1, xl.y + xn.y, p.eta * v[m].y));
+          }
+          v[m] = y;
+        }
+        odd_extend<T>(v, buf, g);
+      } else if (ph == 2 && LAST) {
+        const PencilConsts kc = make_consts(p, pc);
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (!T::lower(r)) continue;
+          const int k = T::rowk(g, r);
+          double2 wv = make_double2(0.0, 0.0);
+          if (k >= 1) {
+            const double2 lam = spec_pair(p, kc, k);
+            wv.x = pc.vp ? (-v[r].y * hs) / lam.x : 0.0;
+            wv.y = pc.vq ? (v[r].x * hs) / lam.y : 0.0;
+          }
+          buf[k] = wv;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+          const int j = g + G * m;
+          if (m < E / 2) {
+            v[m] = buf[j];
+          } else {
+            const double2 tt = (j == N) ? make_double2(0.0, 0.0) : buf[L - j];
+            v[m] = make_double2(-tt.x, -tt.y);
+          }
+        }
+      } else {
+        // final DST (row layout) -> Y
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < E; ++r) {
+          if (!T::lower(r)) continue;
+          buf[oswz(T::rowk(g, r), w)] = make_double2(-v[r].y * hs, v[r].x * hs);
+        }
+        if (p.contiguous) {
+          __syncwarp();
+          for (int j = g + 1; j <= p.n; j += 32) {
+            const double2 yv = buf[oswz(j, w)];
+            if (RSFDE_TILE_SKIP & 2) continue;
+            if (pc.vp) p.Y[pc.off_p + j - 1] = yv.x;
+            if (pc.vq) p.Y[pc.off_q + j - 1] = yv.y;
+          }
+          __syncwarp();
+        } else {
+          compute_bar();
+          const long long base = tile_base(p, t);
+          for (int e = threadIdx.x; e < p.n * kTilePairs; e += 32 * kTilePairs) {
+            const int row = e / kTilePairs, q = e % kTilePairs;
+            const int vm = tvalid[q];
+            if (!(vm & 1)) continue;
+            const double2 yv = bufs[q * L + oswz(row + 1, q)];
+            double* dst = p.Y + base + (long long)row * p.stride + 2 * q;
+            if (RSFDE_TILE_SKIP & 2) continue;
+              if (vm & 2) *reinterpret_cast<double2*>(dst) = yv;
+            else *dst = yv.x;
+          }
+          compute_bar();
+        }
+      }
+    }
+  }
+}
+
+// host: tensor map of one input vector for this pass (see the stage layout above)
+static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtensorMap* tm) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q);
+    if (err != cudaSuccess || q != cudaDriverEntryPointSuccess || !encode) return cudaErrorNotSupported;
+  }
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], es[3] = {1, 1, 1};
+  CUtensorMapSwizzle swz;
+  if (p.contiguous) {
+    dims[0] = (cuuint64_t)p.geo.P; dims[1] = (cuuint64_t)(p.geo.NP / p.geo.P); dims[2] = 1;
+    strides[0] = dims[0] * 8; strides[1] = dims[0] * dims[1] * 8;
+    box[0] = kBoxRows; box[1] = kTilePencils; box[2] = 1;
+    swz = CU_TENSOR_MAP_SWIZZLE_NONE;
+  } else {
+    dims[0] = (cuuint64_t)p.inner; dims[1] = (cuuint64_t)p.n; dims[2] = (cuuint64_t)(p.geo.NP / ((long long)p.n * p.inner));
+    strides[0] = dims[0] * 8; strides[1] = dims[0] * dims[1] * 8;
+    box[0] = kTilePencils; box[1] = kBoxRows; box[2] = 1;
+    swz = kTilePairs == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  }
+  const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int MODE>
+cudaError_t launch_tile(const PassParams& p, cudaStream_t s) {
+  constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
+  const size_t smem = (size_t)kTilePairs * 1024 * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
+  static int sms = 0;
+  if (!sms) {
+    cudaError_t err = cudaFuncSetAttribute(tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  alignas(64) CUtensorMap tmR, tmX;
+  memset(&tmR, 0, sizeof(tmR));
+  memset(&tmX, 0, sizeof(tmX));
+  cudaError_t err = cudaSuccess;
+  if (OPER) err = tile_tensor_map(p, p.R, &tmR);
+  if (err == cudaSuccess && (!OPER || p.xmode == X_INPUT)) err = tile_tensor_map(p, p.X, &tmX);
+  if (err != cudaSuccess) return err;
+  const long long ntiles = p.contiguous ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
+  const long long blocks = ntiles < (long long)kCtasPerSm * sms ? ntiles : (long long)kCtasPerSm * sms;
+  tile_kernel<MODE><<<(unsigned)blocks, kTileThreads, smem, s>>>(p, tmR, tmX);
+  err = cudaGetLastError();
+  if (err != cudaSuccess && getenv("RSFDE_DEBUG")) {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, tile_kernel<MODE>);
+    fprintf(stderr, "tile_kernel<%d>: regs %d maxthreads %d static %zu maxdyn %d local %zu smem %zu blocks %lld\n", MODE,
+            a.numRegs, a.maxThreadsPerBlock, a.sharedSizeBytes, a.maxDynamicSharedSizeBytes, a.localSizeBytes, smem,
+            blocks);
+  }
+  return err;
+}
+
+}  // namespace rsfde

@@ -55,7 +55,10 @@ def _prob(kind, shape, M=4):
 SHAPES = [("c1", (255,)), ("c1", (7,)), ("c1", (1,)), ("c5", (31, 63)), ("c5", (255, 15)),
           ("c5", (15, 7, 31)), ("c5", (63, 63, 63)), ("ex", (3, 3, 3)), ("c5", (1, 3, 1)),
           # long pencils: the three-stage FFT (L = 2048, 4096), strided and contiguous axes
-          ("c5", (2047, 7)), ("c5", (7, 2047)), ("c5", (3, 1023, 3)), ("c1", (2047,))]
+          ("c5", (2047, 7)), ("c5", (7, 2047)), ("c5", (3, 1023, 3)), ("c1", (2047,)),
+          # n = 511 pencils: the warp-specialised tile pipeline (strided tiles of 16 pencils, a
+          # ragged last tile, the pad column, and contiguous 16-row tiles)
+          ("c5", (511, 15, 31)), ("c5", (15, 511, 7)), ("c5", (7, 15, 511)), ("c5", (511, 511)), ("c1", (511,))]
 
 
 @pytest.fixture(scope="module")

@@ -15,6 +15,10 @@ from paper_2404_10221_b200 import _lib as L
 from paper_2404_10221_b200 import inputs as I
 from paper_2404_10221_b200.solver import RsfdeSolver
 
+if "--lib" in sys.argv:  # experiment variant of the library (tools/tile_variants.sh)
+    i = sys.argv.index("--lib")
+    L.load(sys.argv[i + 1])
+    del sys.argv[i:i + 2]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 511
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 prob = I.config_c5(n=n)
