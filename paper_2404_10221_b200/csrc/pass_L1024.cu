@@ -5,18 +5,42 @@ namespace rsfde {
 using T1024 = Lay2<32, 32>;
 RSFDE_INSTANTIATE_T(T1024)
 
-static bool tile_ok(const PassParams& p) {
-  if (p.flags & PASS_FLAG_NO_PIPE) return false;
-  return p.contiguous || (p.inner % kTilePencils == 0);  // a strided tile = adjacent pencils of one block
+// tile width: 128-byte rows where rows are >= 2 MB apart, else 64-byte rows (two CTAs per SM);
+// 0 = no tile pipeline (a strided tile must be adjacent pencils of one block)
+static int tile_pairs(const PassParams& p) {
+  if (p.flags & PASS_FLAG_NO_PIPE) return 0;
+  if (p.contiguous) return 4;
+  // (128-byte rows, TP = 8, measured no faster on the 2 MB-stride axis inside the full pass: the
+  //  FFT work, not the row-piece count, sets the pace there)
+  return p.inner % 8 == 0 ? 4 : 0;
+}
+
+template <int MODE>
+static cudaError_t launch_tile_any(const PassParams& p, int tp, cudaStream_t s) {
+  (void)tp;  // only 64-byte tiles are instantiated (see tile_pairs)
+  return launch_tile<MODE, 4>(p, s);
 }
 
 cudaError_t launch_oper_1024(const PassParams& p, bool spectral, bool last, cudaStream_t s) {
-  if (spectral && tile_ok(p)) return last ? launch_tile<MODE_OPER_SPEC_LAST>(p, s) : launch_tile<MODE_OPER_SPEC>(p, s);
+  const int tp = tile_pairs(p);
+  if (spectral && tp) return last ? launch_tile_any<MODE_OPER_SPEC_LAST>(p, tp, s) : launch_tile_any<MODE_OPER_SPEC>(p, tp, s);
   return launch_oper_t<T1024>(p, spectral, last, s);
 }
 
 cudaError_t launch_dst_1024(const PassParams& p, bool last, cudaStream_t s) {
-  if (tile_ok(p)) return last ? launch_tile<MODE_DST_LAST>(p, s) : launch_tile<MODE_DST>(p, s);
+  const int tp = tile_pairs(p);
+  if (tp) return last ? launch_tile_any<MODE_DST_LAST>(p, tp, s) : launch_tile_any<MODE_DST>(p, tp, s);
   return launch_dst_t<T1024>(p, last, s);
 }
 }  // namespace rsfde
+
+#if RSFDE_TILE_TRACE
+extern "C" int rsfde_debug_tile_trace_select(int launch) {
+  int zero = 0;
+  cudaMemcpyToSymbol(rsfde::g_trace_launch, &zero, sizeof(int));
+  return (int)cudaMemcpyToSymbol(rsfde::g_trace_target, &launch, sizeof(int));
+}
+extern "C" int rsfde_debug_tile_trace(void* host) {
+  return (int)cudaMemcpyFromSymbol(host, rsfde::g_tile_trace, sizeof(rsfde::g_tile_trace));
+}
+#endif

@@ -58,18 +58,21 @@ struct PencilConsts {
   double cP_p, cP_q;       // sum_{i != axis} eta_i q_i / lambda^H_i
 };
 
-// coordinates (0-based) of a pencil; entry [axis] = 0
+// coordinates (0-based) of a pencil; entry [axis] = 0.  Pencil indices stay below 2^23 (every
+// n_i + 1 <= 2048), so the index arithmetic is 32-bit (a 64-bit division costs ~10x more).
 __device__ __forceinline__ void pencil_coords(const PassParams& p, long long idx, int& c0, int& c1, int& c2) {
   const Geom& G = p.geo;
+  const unsigned u = (unsigned)idx;
   c0 = c1 = c2 = 0;
   if (p.contiguous) {
-    if (G.d == 3) { c0 = (int)(idx / G.n[1]); c1 = (int)(idx % G.n[1]); }
-    else if (G.d == 2) { c0 = (int)idx; }
+    if (G.d == 3) { c0 = (int)(u / (unsigned)G.n[1]); c1 = (int)(u % (unsigned)G.n[1]); }
+    else if (G.d == 2) { c0 = (int)u; }
   } else {
-    const long long o = idx / p.inner;
-    const long long i = idx % p.inner;
+    const unsigned inner = (unsigned)p.inner;
+    const unsigned o = u / inner;
+    const unsigned i = u - o * inner;
     if (G.d == 3) {
-      if (p.axis == 0) { c1 = (int)(i / G.P); c2 = (int)(i % G.P); }
+      if (p.axis == 0) { c1 = (int)(i / (unsigned)G.P); c2 = (int)(i % (unsigned)G.P); }
       else { c0 = (int)o; c2 = (int)i; }
     } else {
       c1 = (int)i;
@@ -127,8 +130,9 @@ __device__ __forceinline__ PairCtx make_pair(const PassParams& p, long long pair
     pc.vq = active && r1 < rows && pencil_inside(p, b0, b1, b2);
   } else {
     const long long pen = 2 * pair;  // even pencil index; inner is even
-    const long long o = pen / p.inner, i = pen % p.inner;
-    pc.off_p = o * (long long)p.n * p.inner + i;
+    const unsigned inner = (unsigned)p.inner;
+    const unsigned o = (unsigned)pen / inner, i = (unsigned)pen - o * inner;
+    pc.off_p = (long long)o * p.n * p.inner + i;
     pc.off_q = pc.off_p + 1;
     pc.pen_p = pen;
     pc.pen_q = pen + 1;
@@ -183,8 +187,9 @@ __device__ __forceinline__ void st_pair(const PassParams& p, double* X, const Pa
 __device__ __forceinline__ double2 e_pair(const PassParams& p, const PairCtx& pc, const PencilConsts& kc, int j) {
   const ECoef& E = p.e;
   if (E.kind == 2) {
-    long long st = 1;  // dense stride of the axis
-    for (int i = p.axis + 1; i < p.geo.d; ++i) st *= p.geo.n[i];
+    // dense stride of the axis (d <= 3: at most two later axes)
+    const long long st = (p.axis + 1 < p.geo.d ? (long long)p.geo.n[p.axis + 1] : 1ll) *
+                         (p.axis + 2 < p.geo.d ? (long long)p.geo.n[p.axis + 2] : 1ll);
     const long long o = (long long)(j - 1) * st;
     return make_double2(pc.vp ? __ldg(E.grid + kc.eoff_p + o) : 0.0, pc.vq ? __ldg(E.grid + kc.eoff_q + o) : 0.0);
   }

@@ -28,17 +28,44 @@ namespace rsfde {
 #ifndef RSFDE_TILE_SKIP
 #define RSFDE_TILE_SKIP 0
 #endif
+#ifndef RSFDE_TILE_TRACE  // experiments only: per-tile clock64 stamps of warp 0 of every CTA
+#define RSFDE_TILE_TRACE 0
+#endif
+#if RSFDE_TILE_TRACE
+__device__ unsigned long long g_tile_trace[512][32][8];
+__device__ int g_trace_launch = 0, g_trace_target = -1;  // launch counter / launch to record (-1: every one)
+#define TTRACE(slot)                                                                                   \
+  if (threadIdx.x == 0 && blockIdx.x < 512 && tcount < 32 &&                                           \
+      (g_trace_target < 0 || g_trace_target == trace_launch)) {                                        \
+    unsigned smid;                                                                                     \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                                \
+    g_tile_trace[blockIdx.x][tcount][slot] = clock64();                                                \
+    g_tile_trace[blockIdx.x][tcount][7] = smid;                                                        \
+  }
+#else
+#define TTRACE(slot)
+#endif
 
-constexpr int kTilePairs = 4;                        // pencil pairs per tile (one compute warp each)
-constexpr int kTilePencils = 2 * kTilePairs;          // adjacent pencils per tile
-constexpr int kRowBytes = 8 * kTilePencils;           // bytes of one tile row on a strided axis
-// 3 warpgroups: warpgroups 0-1 = the 8 compute warps, warpgroup 2 = the producer warp (+3 idle
-// warps).  The producer warpgroup gives its registers to the compute warps (setmaxnreg): launched at
-// 168 registers/thread, compute warps run at 232 (no spills), the producer at 40.
-constexpr int kTileThreads = kTilePairs == 8 ? 384 : 256;
-constexpr int kCtasPerSm = kTilePairs == 8 ? 1 : 2;
+// Tile width TP pencil pairs (one compute warp each): TP = 8 -> 16 pencils = 128-byte rows, one CTA
+// of 12 warps per SM; TP = 4 -> 64-byte rows, two CTAs of 8 warps per SM.  128-byte rows are
+// needed on axes whose rows are >= 2 MB apart (every row piece is then its own 2 MB page, and TMA
+// throughput is set by the number of row pieces: tools/micro/tma_micro.cu, 3.0 vs 5.9 TB/s).
+template <int TP>
+struct TileCfg {
+  static constexpr int kTilePencils = 2 * TP;                       // adjacent pencils per tile
+  static constexpr int kRowBytes = 8 * kTilePencils;                // bytes of one tile row
+  static constexpr int kTileThreads = TP == 8 ? 384 : 256;
+  static constexpr int kCtasPerSm = TP == 8 ? 1 : 2;
+  static constexpr int kComputeRegs = TP == 8 ? 232 : 216;
+};
 constexpr int kProducerRegs = 40;
-constexpr int kComputeRegs = kTilePairs == 8 ? 232 : 216;
+constexpr int kBoxRows = 256;
+#define RSFDE_TILE_CONSTS                                              \
+  constexpr int kTilePairs = TP;                                       \
+  constexpr int kTilePencils = TileCfg<TP>::kTilePencils;              \
+  constexpr int kRowBytes = TileCfg<TP>::kRowBytes;                    \
+  constexpr size_t kStageBytes = 2 * (size_t)kBoxRows * kRowBytes;     \
+  (void)kTilePairs; (void)kTilePencils; (void)kRowBytes; (void)kStageBytes;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -70,14 +97,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kTilePairs) : "memory"); }
+template <int TP>
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TP) : "memory"); }
 
 // element offset of the first pencil of tile t (strided: pencil 16t; contiguous: row 16t)
+template <int TP, bool CT>
 __device__ __forceinline__ long long tile_base(const PassParams& p, long long t) {
-  if (p.contiguous) return kTilePencils * t * p.geo.P;
-  const long long pen = kTilePencils * t;
-  const long long o = pen / p.inner, i = pen % p.inner;
-  return o * (long long)p.n * p.inner + i;
+  RSFDE_TILE_CONSTS
+  if (CT) return kTilePencils * t * p.geo.P;
+  const unsigned pen = (unsigned)(kTilePencils * t), inner = (unsigned)p.inner;
+  const unsigned o = pen / inner, i = pen - o * inner;
+  return (long long)o * p.n * p.inner + i;
 }
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2,
@@ -93,28 +123,40 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 // box {16, 256, 1} with the 128-byte swizzle -> stage row r (axis position r + 1) holds the 16
 // pencils of the tile as 8 chunks of 16 bytes (one per pair), chunk w stored at w ^ (r & 7).
 // Contiguous axis: tensor map {P, rows}, box {256, 16} -> stage[half][row][256].
-constexpr int kBoxRows = 256;
-constexpr size_t kStageBytes = 2 * kBoxRows * kRowBytes;  // both layouts, n <= 511
 
 // producer: one lane streams one tile input into the stage (two box copies)
+template <int TP, bool CT>
 __device__ __forceinline__ void produce(const PassParams& p, const CUtensorMap* tm, long long t, char* stage,
                                         unsigned long long* full) {
+  RSFDE_TILE_CONSTS
   mbar_expect_tx(full, (unsigned)kStageBytes);
-  if (p.contiguous) {
+  if (CT) {
     tma_load_3d(stage, tm, 0, (int)(kTilePencils * t), 0, full);
     tma_load_3d(stage + kStageBytes / 2, tm, kBoxRows, (int)(kTilePencils * t), 0, full);
   } else {
-    const long long pen = kTilePencils * t;
-    const int o = (int)(pen / p.inner), i = (int)(pen % p.inner);
+    const unsigned pen = (unsigned)(kTilePencils * t), inner = (unsigned)p.inner;
+    const int o = (int)(pen / inner), i = (int)(pen - (unsigned)o * inner);
     tma_load_3d(stage, tm, i, 0, o, full);
     tma_load_3d(stage + kStageBytes / 2, tm, i, kBoxRows, o, full);
   }
 }
 
+// 1/x to ~1 ulp: hardware approximation + two Newton steps (instead of a full IEEE division)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // value pair (p, q) of compute warp w at axis position j (1..n) from the stage
+template <int TP, bool CT>
 __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* stage, int w, int j) {
+  RSFDE_TILE_CONSTS
   const int r = j - 1;
-  if (p.contiguous) {
+  if (CT) {
     const double* s = reinterpret_cast<const double*>(stage) + (r >> 8) * (kTilePencils * kBoxRows) + (r & 255);
     return make_double2(s[(2 * w) * kBoxRows], s[(2 * w + 1) * kBoxRows]);
   }
@@ -127,9 +169,10 @@ __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* s
 // conflict-free across the 8 buffers
 __device__ __forceinline__ int oswz(int k, int w) { return k ^ (w & 7); }
 
-template <int MODE>
-__global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR,
+template <int MODE, int TP, bool CT>
+__global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasPerSm) tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR,
                                                           const __grid_constant__ CUtensorMap tmX) {
+  RSFDE_TILE_CONSTS
   using T = Lay2<32, 32>;
   constexpr int E = 32, G = 32, L = 1024, N = 512;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
@@ -141,7 +184,7 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
   __shared__ __align__(8) unsigned long long full_bar, empty_bar;
   __shared__ int tvalid[kTilePairs];  // validity bits (p, q) of each warp's pair in the current tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long ntiles = p.contiguous ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
+  const long long ntiles = CT ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
   const int jobs_per_tile = OPER ? (p.xmode == X_ZERO ? 1 : 2) : 1;
   if (threadIdx.x == 0) {
     mbar_init(&full_bar, 1);
@@ -159,7 +202,7 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
       for (int k = 0; k < jobs_per_tile; ++k, ++job) {
         if (job > 0) mbar_wait(&empty_bar, (unsigned)((job - 1) & 1));
         const CUtensorMap* src = OPER ? ((k == 0 || p.xmode == X_E_TIMES_R) ? &tmR : &tmX) : &tmX;
-        if (lane == 0) produce(p, src, t, stage, &full_bar);
+        if (lane == 0) produce<TP, CT>(p, src, t, stage, &full_bar);
         __syncwarp();
       }
     }
@@ -167,27 +210,46 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
   }
 
   // -------------------------------------------------------------------- compute warps
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kComputeRegs));
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(TileCfg<TP>::kComputeRegs));
+  // separable e(x, t) along the pass axis (X = E o R): the axis factors g_a, k_a in shared memory
+  __shared__ double e_ga[N], e_ka[N];
+  const bool e_tab = OPER && p.xmode == X_E_TIMES_R && p.e.kind != 2;
+  if (e_tab) {
+    const double* ga = p.e.g[p.axis];
+    const double* ka = p.e.k[p.axis];
+    for (int j = threadIdx.x; j < N; j += 32 * kTilePairs) {
+      e_ga[j] = (ga && j < p.n) ? __ldg(ga + j) : 1.0;
+      e_ka[j] = (ka && j < p.n) ? __ldg(ka + j) : 0.0;
+    }
+    compute_bar<TP>();
+  }
   const int w = warp, g = lane;
   double2* buf = bufs + w * L;
   const double rs = p.rscale ? __ldg(p.rscale) : 1.0;
   const double hs = 0.5 * p.dst_scale;
   long long job = 0;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  int tcount = 0;
+  (void)tcount;
+#if RSFDE_TILE_TRACE
+  const int trace_launch = *(volatile int*)&g_trace_launch;
+#endif
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
     const long long pair = (long long)kTilePairs * t + w;
     const bool active = pair < p.npairs;
     const PairCtx pc = make_pair(p, active ? pair : 0, active);
     if (lane == 0) tvalid[w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
     double2 v[E];
+    TTRACE(0)
     // ---- job 0: primary input
     mbar_wait(&full_bar, (unsigned)(job & 1));
+    TTRACE(1)
     if (OPER) {
 #pragma unroll
       for (int m = 0; m < E; ++m) {
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
         if (m < E / 2 && j >= 1 && j <= p.n) {
-          r = stage_pair(p, stage, w, j);
+          r = stage_pair<TP, CT>(p, stage, w, j);
           r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
         }
         v[m] = r;
@@ -198,7 +260,7 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
         if (j >= 1 && j <= p.n) {
-          r = stage_pair(p, stage, w, j);
+          r = stage_pair<TP, CT>(p, stage, w, j);
           r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
         }
         v[m] = r;
@@ -212,9 +274,23 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
     const int first = OPER ? 0 : 2;
     const int last_phase = LAST ? 3 : 2;
 #pragma unroll 1
-    for (int ph = first; ph <= last_phase; ++ph) {
-      if (!(RSFDE_TILE_SKIP & 1)) T::fft(v, buf, g, p.tw, ph == 1);
-      if (ph == 0) {
+    for (int ph0 = first; ph0 <= last_phase; ++ph0) {
+      // One FFT body per kernel: the phase index is made opaque to the compiler (otherwise it clones
+      // the loop body per phase, 4 FFT bodies = 270 KB of SASS and instruction-cache stalls), and the
+      // inverse transform is conj(FFT(conj(.))), which for E == G maps the row layout to the column
+      // layout exactly like fft_inv.
+      int ph;
+      asm volatile("mov.b32 %0, %1;" : "=r"(ph) : "r"(ph0));
+      const unsigned long long cmsk = (ph == 1) ? 0x8000000000000000ull : 0ull;
+      if (!(RSFDE_TILE_SKIP & 1)) {
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
+        fft_fwd<E, G>(v, buf, g, p.tw);
+#pragma unroll
+        for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
+      }
+      TTRACE(2 + ph)
+      if (OPER && ph == 0) {
         // C = S H R = s lambda^H D(R) (non-last spectral pass), via the partner spectrum
         if (!LAST) {
           __syncwarp();
@@ -237,7 +313,7 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
             buf[oswz(T::rowk(g, r), w)] = cv[i++];
           }
           // store C
-          if (p.contiguous) {
+          if (CT) {
             __syncwarp();
             for (int j = g + 1; j <= p.n; j += 32) {
               const double2 c = buf[oswz(j, w)];
@@ -247,8 +323,8 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
             }
             __syncwarp();
           } else {
-            compute_bar();
-            const long long base = tile_base(p, t);
+            compute_bar<TP>();
+            const long long base = tile_base<TP, CT>(p, t);
             for (int e = threadIdx.x; e < p.n * kTilePairs; e += 32 * kTilePairs) {
               const int row = e / kTilePairs, q = e % kTilePairs;
               const double2 c = bufs[q * L + oswz(row + 1, q)];
@@ -259,12 +335,12 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
               if (vm & 2) *reinterpret_cast<double2*>(dst) = c;
               else *dst = c.x;
             }
-            compute_bar();
+            compute_bar<TP>();
           }
         }
 #pragma unroll
         for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
-      } else if (ph == 1) {
+      } else if (OPER && ph == 1) {
         // X channel from the stage (job 1) into the pair buffer (x = X, or e o R), then
         // y = H X + eta T R on j = g + G m with the stencil neighbours from the buffer
         const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
@@ -275,9 +351,16 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
           const int j = g + G * m;
           double2 x = make_double2(0.0, 0.0);
           if (p.xmode != X_ZERO && j >= 1 && j <= p.n) {
-            x = stage_pair(p, stage, w, j);
+            x = stage_pair<TP, CT>(p, stage, w, j);
             if (p.xmode == X_E_TIMES_R) {
-              const double2 e = e_pair(p, pc, kc, j);
+              double2 e;
+              if (e_tab) {
+                const double ga = e_ga[j - 1], ka = e_ka[j - 1];
+                e = make_double2(fma(p.e.b * kc.eP_p, ga, p.e.a) + (kc.eK_p + ka),
+                                 fma(p.e.b * kc.eP_q, ga, p.e.a) + (kc.eK_q + ka));
+              } else {
+                e = e_pair(p, pc, kc, j);
+              }
               x = make_double2(rs * x.x * e.x, rs * x.y * e.y);
             }
             if (!pc.vp) x.x = 0.0;
@@ -305,17 +388,42 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
         }
         odd_extend<T>(v, buf, g);
       } else if (ph == 2 && LAST) {
+        // S y (row layout, k = g + G r for r < E/2) into the pair buffer, then Lambda^{-1} in a rolled
+        // loop over the same k (small code: the spectrum kinds are a runtime switch)
         const PencilConsts kc = make_consts(p, pc);
+        const Spec& S = p.spec;
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < E; ++r) {
           if (!T::lower(r)) continue;
-          const int k = T::rowk(g, r);
+          buf[T::rowk(g, r)] = make_double2(-v[r].y * hs, v[r].x * hs);
+        }
+        // Lambda = (ebar + cP + tq_k) cH lh_k (P_hat) | (ebar + cP + tq_k) (P_alpha) | cH lh_k (H):
+        // one fast reciprocal per value instead of an IEEE division
+        const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
+        const double icHp = (S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_p;
+        const double icHq = (S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_q;
+#pragma unroll 1
+        for (int m = 0; m < E / 2; ++m) {
+          const int k = g + G * m;
           double2 wv = make_double2(0.0, 0.0);
           if (k >= 1) {
-            const double2 lam = spec_pair(p, kc, k);
-            wv.x = pc.vp ? (-v[r].y * hs) / lam.x : 0.0;
-            wv.y = pc.vq ? (v[r].x * hs) / lam.y : 0.0;
+            const double2 z = buf[k];
+            if (fast) {
+              const double lh = (S.kind == SPEC_PALPHA) ? 1.0 : __ldg(S.lamH[p.axis] + k - 1);
+              double lp = 1.0, lq = 1.0;
+              if (S.kind != SPEC_HINV) {
+                const double tq = __ldg(S.tq[p.axis] + k - 1);
+                lp = S.ebar + kc.cP_p + tq;
+                lq = S.ebar + kc.cP_q + tq;
+              }
+              wv.x = pc.vp ? z.x * (rcp_nr(lp * lh) * icHp) : 0.0;
+              wv.y = pc.vq ? z.y * (rcp_nr(lq * lh) * icHq) : 0.0;
+            } else {
+              const double2 lam = spec_pair(p, kc, k);
+              wv.x = pc.vp ? z.x / lam.x : 0.0;
+              wv.y = pc.vq ? z.y / lam.y : 0.0;
+            }
           }
           buf[k] = wv;
         }
@@ -338,7 +446,7 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
           if (!T::lower(r)) continue;
           buf[oswz(T::rowk(g, r), w)] = make_double2(-v[r].y * hs, v[r].x * hs);
         }
-        if (p.contiguous) {
+        if (CT) {
           __syncwarp();
           for (int j = g + 1; j <= p.n; j += 32) {
             const double2 yv = buf[oswz(j, w)];
@@ -348,8 +456,8 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
           }
           __syncwarp();
         } else {
-          compute_bar();
-          const long long base = tile_base(p, t);
+          compute_bar<TP>();
+          const long long base = tile_base<TP, CT>(p, t);
           for (int e = threadIdx.x; e < p.n * kTilePairs; e += 32 * kTilePairs) {
             const int row = e / kTilePairs, q = e % kTilePairs;
             const int vm = tvalid[q];
@@ -360,15 +468,25 @@ __global__ void __launch_bounds__(kTileThreads, kCtasPerSm) tile_kernel(const Pa
               if (vm & 2) *reinterpret_cast<double2*>(dst) = yv;
             else *dst = yv.x;
           }
-          compute_bar();
+          compute_bar<TP>();
         }
       }
     }
+    TTRACE(6)
   }
+#if RSFDE_TILE_TRACE
+  // count launches (the last compute thread to finish bumps the counter once per launch)
+  __shared__ int done_warps;
+  if (threadIdx.x == 0) done_warps = 0;
+  compute_bar<TP>();
+  if (lane == 0 && atomicAdd(&done_warps, 1) == 0 && blockIdx.x == 0) atomicAdd(&g_trace_launch, 1);
+#endif
 }
 
 // host: tensor map of one input vector for this pass (see the stage layout above)
+template <int TP>
 static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtensorMap* tm) {
+  RSFDE_TILE_CONSTS
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -395,13 +513,15 @@ static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtenso
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int MODE>
-cudaError_t launch_tile(const PassParams& p, cudaStream_t s) {
+template <int MODE, int TP, bool CT>
+cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
+  RSFDE_TILE_CONSTS
+  constexpr int kTileThreads = TileCfg<TP>::kTileThreads, kCtasPerSm = TileCfg<TP>::kCtasPerSm;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
   const size_t smem = (size_t)kTilePairs * 1024 * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
   static int sms = 0;
   if (!sms) {
-    cudaError_t err = cudaFuncSetAttribute(tile_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t err = cudaFuncSetAttribute(tile_kernel<MODE, TP, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -411,21 +531,27 @@ cudaError_t launch_tile(const PassParams& p, cudaStream_t s) {
   memset(&tmR, 0, sizeof(tmR));
   memset(&tmX, 0, sizeof(tmX));
   cudaError_t err = cudaSuccess;
-  if (OPER) err = tile_tensor_map(p, p.R, &tmR);
-  if (err == cudaSuccess && (!OPER || p.xmode == X_INPUT)) err = tile_tensor_map(p, p.X, &tmX);
+  if (OPER) err = tile_tensor_map<TP>(p, p.R, &tmR);
+  if (err == cudaSuccess && (!OPER || p.xmode == X_INPUT)) err = tile_tensor_map<TP>(p, p.X, &tmX);
   if (err != cudaSuccess) return err;
   const long long ntiles = p.contiguous ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
   const long long blocks = ntiles < (long long)kCtasPerSm * sms ? ntiles : (long long)kCtasPerSm * sms;
-  tile_kernel<MODE><<<(unsigned)blocks, kTileThreads, smem, s>>>(p, tmR, tmX);
+  tile_kernel<MODE, TP, CT><<<(unsigned)blocks, kTileThreads, smem, s>>>(p, tmR, tmX);
   err = cudaGetLastError();
   if (err != cudaSuccess && getenv("RSFDE_DEBUG")) {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, tile_kernel<MODE>);
+    cudaFuncGetAttributes(&a, tile_kernel<MODE, TP, CT>);
     fprintf(stderr, "tile_kernel<%d>: regs %d maxthreads %d static %zu maxdyn %d local %zu smem %zu blocks %lld\n", MODE,
             a.numRegs, a.maxThreadsPerBlock, a.sharedSizeBytes, a.maxDynamicSharedSizeBytes, a.localSizeBytes, smem,
             blocks);
   }
   return err;
+}
+
+// contiguous (last-axis) and strided tiles are separate kernels (smaller code, fewer branches)
+template <int MODE, int TP>
+cudaError_t launch_tile(const PassParams& p, cudaStream_t s) {
+  return p.contiguous ? launch_tile_ct<MODE, TP, true>(p, s) : launch_tile_ct<MODE, TP, false>(p, s);
 }
 
 }  // namespace rsfde

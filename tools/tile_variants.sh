@@ -15,4 +15,9 @@ for v in 1 2 3; do
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $OUT/librsfde_skip$v.so $OBJS \
     $OUT/pass_L1024_$v.o -lrt -ldl -lpthread
 done
+# per-tile clock64 trace variant (tools/tile_trace.py)
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC -DRSFDE_TILE_TRACE=1 \
+  -I paper_2404_10221_b200/csrc -I include -c paper_2404_10221_b200/csrc/pass_L1024.cu -o $OUT/pass_L1024_trace.o
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $OUT/librsfde_trace.so $OBJS \
+  $OUT/pass_L1024_trace.o -lrt -ldl -lpthread
 ls $OUT
