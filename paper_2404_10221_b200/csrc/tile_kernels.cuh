@@ -32,7 +32,7 @@ namespace rsfde {
 #define RSFDE_TILE_TRACE 0
 #endif
 #if RSFDE_TILE_TRACE
-__device__ unsigned long long g_tile_trace[512][32][8];
+__device__ unsigned long long g_tile_trace[512][32][12];
 __device__ int g_trace_launch = 0, g_trace_target = -1;  // launch counter / launch to record (-1: every one)
 #define TTRACE(slot)                                                                                   \
   if (threadIdx.x == 0 && blockIdx.x < 512 && tcount < 32 &&                                           \
@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
   // -------------------------------------------------------------------- compute warps
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(TileCfg<TP>::kComputeRegs));
   // separable e(x, t) along the pass axis (X = E o R): the axis factors g_a, k_a in shared memory
+  // (last axis: the same arrays hold the spectrum tables lambda^H_k and tq_k of the axis)
   __shared__ double e_ga[N], e_ka[N];
   const bool e_tab = OPER && p.xmode == X_E_TIMES_R && p.e.kind != 2;
   if (e_tab) {
@@ -220,6 +221,15 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
     for (int j = threadIdx.x; j < N; j += 32 * kTilePairs) {
       e_ga[j] = (ga && j < p.n) ? __ldg(ga + j) : 1.0;
       e_ka[j] = (ka && j < p.n) ? __ldg(ka + j) : 0.0;
+    }
+    compute_bar<TP>();
+  }
+  if (LAST && !e_tab) {
+    const double* lh = p.spec.lamH[p.axis];
+    const double* tq = p.spec.tq[p.axis];
+    for (int j = threadIdx.x; j < N; j += 32 * kTilePairs) {
+      e_ga[j] = (lh && j < p.n) ? __ldg(lh + j) : 1.0;
+      e_ka[j] = (tq && j < p.n) ? __ldg(tq + j) : 0.0;
     }
     compute_bar<TP>();
   }
@@ -338,6 +348,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
             compute_bar<TP>();
           }
         }
+        TTRACE(9)
 #pragma unroll
         for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
       } else if (OPER && ph == 1) {
@@ -345,6 +356,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
         // y = H X + eta T R on j = g + G m with the stencil neighbours from the buffer
         const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
         if (p.xmode != X_ZERO) mbar_wait(&full_bar, (unsigned)(job & 1));
+        TTRACE(11)
         __syncwarp();
 #pragma unroll
         for (int m = 0; m < E / 2; ++m) {
@@ -386,6 +398,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
           }
           v[m] = y;
         }
+        TTRACE(10)
         odd_extend<T>(v, buf, g);
       } else if (ph == 2 && LAST) {
         // S y (row layout, k = g + G r for r < E/2) into the pair buffer, then Lambda^{-1} in a rolled
@@ -403,30 +416,41 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
         const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
         const double icHp = (S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_p;
         const double icHq = (S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_q;
-#pragma unroll 1
-        for (int m = 0; m < E / 2; ++m) {
-          const int k = g + G * m;
-          double2 wv = make_double2(0.0, 0.0);
-          if (k >= 1) {
-            const double2 z = buf[k];
-            if (fast) {
-              const double lh = (S.kind == SPEC_PALPHA) ? 1.0 : __ldg(S.lamH[p.axis] + k - 1);
+        if (fast && !e_tab) {
+          // unrolled: the 16 values are independent (a rolled loop serialises the latencies)
+#pragma unroll
+          for (int m = 0; m < E / 2; ++m) {
+            const int k = g + G * m;
+            double2 wv = make_double2(0.0, 0.0);
+            if (k >= 1) {
+              const double2 z = buf[k];
+              const double lh = (S.kind == SPEC_PALPHA) ? 1.0 : e_ga[k - 1];
               double lp = 1.0, lq = 1.0;
               if (S.kind != SPEC_HINV) {
-                const double tq = __ldg(S.tq[p.axis] + k - 1);
+                const double tq = e_ka[k - 1];
                 lp = S.ebar + kc.cP_p + tq;
                 lq = S.ebar + kc.cP_q + tq;
               }
               wv.x = pc.vp ? z.x * (rcp_nr(lp * lh) * icHp) : 0.0;
               wv.y = pc.vq ? z.y * (rcp_nr(lq * lh) * icHq) : 0.0;
-            } else {
+            }
+            buf[k] = wv;
+          }
+        } else {
+#pragma unroll 1
+          for (int m = 0; m < E / 2; ++m) {
+            const int k = g + G * m;
+            double2 wv = make_double2(0.0, 0.0);
+            if (k >= 1) {
+              const double2 z = buf[k];
               const double2 lam = spec_pair(p, kc, k);
               wv.x = pc.vp ? z.x / lam.x : 0.0;
               wv.y = pc.vq ? z.y / lam.y : 0.0;
             }
+            buf[k] = wv;
           }
-          buf[k] = wv;
         }
+        TTRACE(8)
         __syncwarp();
 #pragma unroll
         for (int m = 0; m < E; ++m) {

@@ -29,7 +29,7 @@ lib.rsfde_debug_tile_trace_select(which)
 S.matvec(L.OP_K, x, m=0, out=y)
 torch.cuda.synchronize()
 print("launch", which)
-tr = np.zeros((512, 32, 8), dtype=np.uint64)
+tr = np.zeros((512, 32, 12), dtype=np.uint64)
 lib.rsfde_debug_tile_trace.restype = ctypes.c_int
 lib.rsfde_debug_tile_trace.argtypes = [ctypes.c_void_p]
 assert lib.rsfde_debug_tile_trace(tr.ctypes.data) == 0
@@ -51,6 +51,14 @@ wait = (t1 - t0)[:, 1:][ok]
 fft_ = (tf - t1)[:, 1:][ok]
 rest = (te - tf)[:, 1:][ok]
 nxt = (t0[:, 1:] - te[:, :-1])[ok]
+def seg(a_slot, b_slot):
+    a = tr[:ncta, 1:, b_slot] - tr[:ncta, 1:, a_slot]
+    return a[(tr[:ncta, 1:, b_slot] > 0) & (tr[:ncta, 1:, a_slot] > 0)]
+for nm, a_, b_ in [("fft0 -> C out done", 2, 9), ("C out -> fft1", 9, 3), ("fft1 -> X ready", 3, 11), ("X ready -> stencil", 11, 10),
+                   ("stencil -> fft2", 10, 4), ("fft2 -> Lambda done", 4, 8), ("Lambda -> fft3", 8, 5)]:
+    a = seg(a_, b_)
+    if a.size:
+        print(f"{nm:24s} median {np.median(a):8.0f} clk")
 for name, a in [("tile period", per_tile), ("wait full", wait), ("data->last fft", fft_), ("output+store", rest),
                 ("loop overhead", nxt)]:
     print(f"{name:18s} median {np.median(a):8.0f} clk  mean {a.mean():8.0f}  p90 {np.percentile(a, 90):8.0f}")
