@@ -72,26 +72,29 @@ template <int JP>
 __global__ void __launch_bounds__(256) dots_after_update_kernel(BasisPtrs b, const double* __restrict__ vscale, int J,
                                                                 const double* __restrict__ z,
                                                                 const double* __restrict__ coef,
-                                                                double* __restrict__ partial, long long n) {
+                                                                double* __restrict__ partial, long long n2) {
   __shared__ double cs[kMaxBasis];
   for (int i = threadIdx.x; i < J; i += blockDim.x) cs[i] = coef[i] * vscale[i];
   __syncthreads();
   double acc[JP];
 #pragma unroll
   for (int i = 0; i < JP; ++i) acc[i] = 0.0;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-    double vv[JP];
-    double zz = __ldg(z + e);
+  // two elements per thread (16-byte loads: the scalar version reached 3.6 TB/s, the others 5.5-6)
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long long)gridDim.x * blockDim.x) {
+    double2 vv[JP];
+    double2 zz = __ldg(z2 + e);
 #pragma unroll
     for (int i = 0; i < JP; ++i) {
       if (i < J) {
-        vv[i] = __ldg(b.V[i] + e);
-        zz = fma(-cs[i], vv[i], zz);
+        vv[i] = __ldg(reinterpret_cast<const double2*>(b.V[i]) + e);
+        zz.x = fma(-cs[i], vv[i].x, zz.x);
+        zz.y = fma(-cs[i], vv[i].y, zz.y);
       }
     }
 #pragma unroll
     for (int i = 0; i < JP; ++i)
-      if (i < J) acc[i] = fma(vv[i], zz, acc[i]);
+      if (i < J) acc[i] = fma(vv[i].x, zz.x, fma(vv[i].y, zz.y, acc[i]));
   }
   block_reduce_store<JP>(acc, J, partial, vscale);
 }
@@ -409,7 +412,7 @@ cudaError_t launch_dots_after_update(const double* const* V, const double* vscal
                                      const double* coef, double* partial, long long NP, int nblk, cudaStream_t s) {
   if (J < 1 || J > kMaxBasis) return cudaErrorInvalidValue;
   const unsigned g = grid_for(NP / 2, nblk);  // same block count as the other reductions
-  RSFDE_JP(run_dots_upd, J, g, s, make_basis(V, J), vscale, J, z, coef, partial, NP);
+  RSFDE_JP(run_dots_upd, J, g, s, make_basis(V, J), vscale, J, z, coef, partial, NP / 2);
   return cudaGetLastError();
 }
 
