@@ -147,6 +147,19 @@ rsfde_status rsfde_gmres_step(rsfde_ctx *ctx, int m, const double *b, double *x,
 rsfde_status rsfde_solve_steps(rsfde_ctx *ctx, int m_begin, int m_count, double *u, const double *F, int F_static,
                                const rsfde_gmres_cfg *cfg, rsfde_report *rep, void *stream);
 
+/* Batched march (the alpha / N sweeps of Tables 1-3, as many
+   independent systems at once).  Runs rsfde_solve_steps(ctxs[i], m_begin[i], m_count[i], u[i],
+   F[i], F_static[i], &cfgs[i], &reps[i], streams[i]) for i < count concurrently: one host worker
+   and one CUDA stream per system (streams may be NULL or hold NULL entries: the library then creates
+   and destroys a non-blocking stream for that system and synchronizes it before returning).  The
+   systems must be distinct contexts (RSFDE_E_CONFIG otherwise); each system's results are exactly
+   those of its own rsfde_solve_steps call (same kernels, deterministic reductions).  F and F_static
+   may be NULL (no source / static).  Returns the first failing system's status (the per-system
+   error text is in rsfde_last_error(ctxs[i])); the other systems still run to completion. */
+rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx *const *ctxs, const int *m_begin, const int *m_count,
+                                     double *const *u, const double *const *F, const int *F_static,
+                                     const rsfde_gmres_cfg *cfgs, rsfde_report *reps, void *const *streams);
+
 /* F^{(m+1/2)} from f(., t_{m+1/2}) sampled on the CLOSED grid (n_i + 2 points per axis, dense C
    layout, boundary samples included): F = (prod_l calH_{alpha_l} f) restricted to the interior,
    calH_l g_j = (1 - alpha_l/12) g_j + alpha_l/24 (g_{j-1} + g_{j+1}) (Eq.(2.2)).  This

@@ -54,6 +54,10 @@ SIGNATURES = {
                                    C.POINTER(C.c_int), DP, C.POINTER(C.c_int), C.c_void_p]),
     "rsfde_solve_steps": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int,
                                     C.POINTER(rsfde_gmres_cfg), C.POINTER(rsfde_report), C.c_void_p]),
+    "rsfde_solve_steps_batch": (C.c_int, [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                          C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int),
+                                          C.POINTER(rsfde_gmres_cfg), C.POINTER(rsfde_report),
+                                          C.POINTER(C.c_void_p)]),
     "rsfde_compact_source": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "rsfde_ebar": (C.c_int, [C.c_void_p, DP, DP, DP]),
     "rsfde_table": (C.c_int, [C.c_void_p, C.c_int, C.c_int, DP]),

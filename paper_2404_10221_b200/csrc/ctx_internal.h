@@ -15,6 +15,7 @@ using rsfde::Geom;
 using rsfde::GmresState;
 
 struct rsfde_ctx {
+  int device = 0;  // CUDA device the context lives on (set by setup)
   int d = 0;
   int n[3] = {1, 1, 1};
   double alpha[3] = {2, 2, 2}, kappa[3] = {0, 0, 0};

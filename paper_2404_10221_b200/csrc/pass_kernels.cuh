@@ -528,12 +528,10 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
 template <class T, int MODE>
 cudaError_t launch_mode(const PassParams& p, cudaStream_t s) {
   const size_t smem = (size_t)T::GROUPS * T::L * sizeof(double2);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(pass_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    attr = true;
-  }
+  // once per process (thread-safe static initialisation: batched solves drive several streams)
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(pass_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
   const long long blocks = (p.npairs + T::GROUPS - 1) / T::GROUPS;
   pass_kernel<T, MODE><<<(unsigned)blocks, T::THREADS, smem, s>>>(p);
   return cudaGetLastError();

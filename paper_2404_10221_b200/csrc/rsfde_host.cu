@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ctx_internal.h"
@@ -599,6 +600,7 @@ rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void*
     return RSFDE_E_CUDA;
   }
   rsfde_ctx* c = new rsfde_ctx();
+  cudaGetDevice(&c->device);
   c->d = p->d;
   for (int i = 0; i < 3; ++i) {
     c->n[i] = i < p->d ? p->n[i] : 1;
@@ -887,6 +889,45 @@ rsfde_status rsfde_solve_steps(rsfde_ctx* c, int m_begin, int m_count, double* u
     rep->setup_seconds = c->setup_seconds;
     rep->total_iters = total;
   }
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx* const* ctxs, const int* m_begin, const int* m_count,
+                                     double* const* u, const double* const* F, const int* F_static,
+                                     const rsfde_gmres_cfg* cfgs, rsfde_report* reps, void* const* streams) {
+  if (count < 0 || (count > 0 && (!ctxs || !m_begin || !m_count || !u || !cfgs))) return RSFDE_E_CONFIG;
+  for (int i = 0; i < count; ++i)
+    for (int k = 0; k < i; ++k)
+      if (ctxs[i] == ctxs[k]) {
+        if (ctxs[i]) ctxs[i]->err = "rsfde_solve_steps_batch: a context appears twice in the batch";
+        return RSFDE_E_CONFIG;
+      }
+  std::vector<rsfde_status> st(count, RSFDE_OK);
+  std::vector<cudaStream_t> own(count, nullptr);
+  // one host worker and one stream per system: the independent marches overlap on the device (small
+  // grids leave most SMs idle) and their per-iteration host syncs overlap on the host
+  auto work = [&](int i) {
+    rsfde_ctx* c = ctxs[i];
+    if (!c) { st[i] = RSFDE_E_CONFIG; return; }
+    if (cudaSetDevice(c->device) != cudaSuccess) { st[i] = RSFDE_E_CUDA; return; }
+    void* s = streams ? streams[i] : nullptr;
+    if (!s) {
+      if (cudaStreamCreateWithFlags(&own[i], cudaStreamNonBlocking) != cudaSuccess) { st[i] = RSFDE_E_CUDA; return; }
+      s = own[i];
+    }
+    st[i] = rsfde_solve_steps(c, m_begin[i], m_count[i], u[i], F ? F[i] : nullptr, F_static ? F_static[i] : 1,
+                              &cfgs[i], reps ? &reps[i] : nullptr, s);
+    if (own[i]) cudaStreamSynchronize(own[i]);
+  };
+  std::vector<std::thread> th;
+  th.reserve(count > 0 ? count - 1 : 0);
+  for (int i = 1; i < count; ++i) th.emplace_back(work, i);
+  if (count > 0) work(0);
+  for (auto& t : th) t.join();
+  for (int i = 0; i < count; ++i)
+    if (own[i]) cudaStreamDestroy(own[i]);
+  for (int i = 0; i < count; ++i)
+    if (st[i] != RSFDE_OK) return st[i];
   return RSFDE_OK;
 }
 

@@ -511,12 +511,16 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
 template <int TP>
 static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtensorMap* tm) {
   RSFDE_TILE_CONSTS
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  // driver entry point, fetched once (thread-safe static initialisation)
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
+    void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    cudaError_t err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q);
-    if (err != cudaSuccess || q != cudaDriverEntryPointSuccess || !encode) return cudaErrorNotSupported;
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return cudaErrorNotSupported;
   cuuint64_t dims[3], strides[2];
   cuuint32_t box[3], es[3] = {1, 1, 1};
   CUtensorMapSwizzle swz;
@@ -543,14 +547,17 @@ cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
   constexpr int kTileThreads = TileCfg<TP>::kTileThreads, kCtasPerSm = TileCfg<TP>::kCtasPerSm;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
   const size_t smem = (size_t)kTilePairs * 1024 * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
-  static int sms = 0;
-  if (!sms) {
-    cudaError_t err = cudaFuncSetAttribute(tile_kernel<MODE, TP, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    int dev = 0;
+  // kernel attribute and SM count, once per process (thread-safe static initialisation)
+  static const int sms = [smem]() -> int {
+    if (cudaFuncSetAttribute(tile_kernel<MODE, TP, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return -1;
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  if (sms <= 0) return cudaErrorInvalidValue;
   alignas(64) CUtensorMap tmR, tmX;
   memset(&tmR, 0, sizeof(tmR));
   memset(&tmX, 0, sizeof(tmX));

@@ -218,6 +218,49 @@ class RsfdeSolver:
             pass
 
 
+def solve_steps_batch(solvers, us, Fs=None, F_static=None, m_begin=None, m_count=None, cfgs=None):
+    """rsfde_solve_steps_batch: march several independent systems concurrently (NEXT-4).
+
+    solvers: RsfdeSolver list (distinct contexts); us: their solution vectors (torch CUDA tensors or
+    numpy host arrays, updated in place); Fs / F_static / m_begin / m_count / cfgs: per-system values
+    as for RsfdeSolver.solve_steps.  Returns one report dict per system."""
+    B = len(solvers)
+    if len(us) != B:
+        raise ValueError("one u per solver")
+    lib = solvers[0].lib if B else L.load()
+    Fs = [None] * B if Fs is None else list(Fs)
+    F_static = [True] * B if F_static is None else list(F_static)
+    m_begin = [0] * B if m_begin is None else list(m_begin)
+    m_count = [S.M - mb for S, mb in zip(solvers, m_begin)] if m_count is None else list(m_count)
+    cfgs = [RsfdeSolver.cfg() for _ in range(B)] if cfgs is None else list(cfgs)
+    ctxs = (C.c_void_p * B)(*[S.ctx.value for S in solvers])
+    ub = (C.c_void_p * B)(*[RsfdeSolver._host_or_dev(u).value for u in us])
+    Fb = (C.c_void_p * B)(*[None if F is None else RsfdeSolver._host_or_dev(F).value for F in Fs])
+    fs = (C.c_int * B)(*[1 if f else 0 for f in F_static])
+    mb = (C.c_int * B)(*m_begin)
+    mc = (C.c_int * B)(*m_count)
+    cf = (L.rsfde_gmres_cfg * B)(*cfgs)
+    reps = (L.rsfde_report * B)()
+    bufs = []
+    for i in range(B):
+        n = max(1, m_count[i])
+        its, rr, cv = (C.c_int * n)(), (C.c_double * n)(), (C.c_ubyte * n)()
+        bufs.append((its, rr, cv))
+        reps[i].iters, reps[i].final_relres, reps[i].converged = its, rr, cv
+    st = lib.rsfde_solve_steps_batch(B, ctxs, mb, mc, ub, Fb, fs, cf, reps, None)
+    if st != 0:
+        msgs = [S.lib.rsfde_last_error(S.ctx).decode() for S in solvers]
+        msg = next((m for m in msgs if m), "")
+        raise L.RsfdeError(st, msg)
+    out = []
+    for i in range(B):
+        its, rr, cv = bufs[i]
+        k = m_count[i]
+        out.append({"iters": list(its)[:k], "relres": list(rr)[:k], "converged": [bool(v) for v in cv][:k],
+                    "loop_seconds": reps[i].loop_seconds, "total_iters": reps[i].total_iters})
+    return out
+
+
 class RsfdeTeam:
     """Slab-sharded 3D solver (x_1 slabs over ``nranks`` ranks).
 

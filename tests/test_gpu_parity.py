@@ -293,3 +293,35 @@ def test_two_sided_gmres_step():
     if its != ref.iters:
         ref = oracle_gmres(K, c, Ls.P_alpha_sqrt(ebar, x0), 20, 1e-11, 200, fixed_iters=its)
     assert relerr(_host(xd), Ls.P_alpha_inv_sqrt(ebar, ref.x)) < 1e-9
+
+
+# ----------------------------------------------------------------------- batched marches (NEXT-4)
+def test_batched_march_equals_separate_marches():
+    # rsfde_solve_steps_batch: several independent systems (an alpha / N sweep as in Tables 1-3,
+    # P:528-636) marched concurrently give exactly the results of separate rsfde_solve_steps calls
+    from paper_2404_10221_b200 import solver as SV
+    probs = [I.example(1, 31, 16, (1.3,)), I.example(1, 63, 16, (1.9,)), I.example(2, 15, 8, (1.5, 1.7)),
+             I.config_c5(M=3, nn=(15, 7, 31))]
+    sols = [_solver(p) for p in probs]
+    Fs = []
+    for S, p in zip(sols, probs):
+        steps = [0] if p.source_static else range(p.M)
+        F = torch.stack([S.compact_source(_dev(p.f_closed(p.t_half(m)))) for m in steps])
+        Fs.append(F[0].contiguous() if p.source_static else F)
+    fst = [bool(p.source_static) for p in probs]
+    cfgs = [S.cfg(restart=p.restart, tol=p.tol) for S, p in zip(sols, probs)]
+    u_sep = [_dev(p.psi_interior()) for p in probs]
+    rep_sep = [S.solve_steps(u, F=F, F_static=f, cfg=c) for S, u, F, f, c in zip(sols, u_sep, Fs, fst, cfgs)]
+    u_bat = [_dev(p.psi_interior()) for p in probs]
+    rep_bat = SV.solve_steps_batch(sols, u_bat, Fs=Fs, F_static=fst, cfgs=cfgs)
+    for a, b, ra, rb in zip(u_sep, u_bat, rep_sep, rep_bat):
+        assert ra["iters"] == rb["iters"] and all(rb["converged"])
+        assert torch.equal(a, b)                      # bit-identical: same kernels, deterministic sums
+
+
+def test_batched_march_rejects_duplicate_contexts():
+    from paper_2404_10221_b200 import solver as SV
+    p = I.example(1, 15, 4, (1.5,))
+    S = _solver(p)
+    with pytest.raises(Exception):
+        SV.solve_steps_batch([S, S], [_dev(p.psi_interior()), _dev(p.psi_interior())])
