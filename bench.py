@@ -331,13 +331,17 @@ def run_ours(args):
     if dom:
         d = prof[dom]
         achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
+        # DRAM bytes per launch of this kernel class from the committed ncu --set full capture of the
+        # C5 K chain (profiles/r01_ncu_traffic.json, tools/ncu_traffic.py); null for other workloads
+        traffic, traffic_src = None, None
+        tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        if os.path.exists(tp) and args.workload == "C5":
             with open(tp) as f:
-                traffic = json.load(f).get(args.workload, {}).get(dom)
+                tj = json.load(f)
+            if dom in tj:
+                traffic, traffic_src = tj[dom]["bytes_per_launch"], tj.get("source")
         roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "launches": d["launches"], "mean_launch_ms": d["ms"] / max(1, d["launches"]),
                 "algorithmic_bytes_per_launch": d["bytes"] / max(1, d["launches"])}
     tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
