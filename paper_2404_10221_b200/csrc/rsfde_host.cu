@@ -261,15 +261,25 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
   const double* Xcur = a.Xin;
   const double* Rcur = a.R;
   int buf = 0;
-  for (int ax = 0; ax < d; ++ax) {
-    const bool last = ax == d - 1;
+  // axis order of the chain (the per-axis operators commute, Eq.(Salpha)).  In 3D the chain runs
+  // x_3 (contiguous) first and puts the spectral last pass on x_1, so that one of the two inverse DST
+  // passes is along the contiguous axis (measured 1.4 % faster K chain at 511^3 than x_1 first);
+  // RSFDE_AXIS_ORDER=fwd restores x_1 first.
+  static const bool fwd = getenv("RSFDE_AXIS_ORDER") && !strcmp(getenv("RSFDE_AXIS_ORDER"), "fwd");
+  const bool rev = d == 3 && !fwd;
+  int ord[3] = {0, 1, 2};
+  if (rev)
+    for (int i = 0; i < d; ++i) ord[i] = d - 1 - i;
+  for (int k = 0; k < d; ++k) {
+    const int ax = ord[k];
+    const bool last = k == d - 1;
     PassParams p = rsfde_axis_params(c, ax);
-    p.xmode = ax == 0 ? a.xmode : X_INPUT;
+    p.xmode = k == 0 ? a.xmode : X_INPUT;
     p.X = Xcur;
     p.R = Rcur;
-    p.rscale = ax == 0 ? a.rscale : nullptr;
+    p.rscale = k == 0 ? a.rscale : nullptr;
     p.eta = a.etafac * c->eta[ax];
-    if (ax == 0 && a.xmode == X_E_TIMES_R) p.e = rsfde_ecoef_at(c, a.m);
+    if (k == 0 && a.xmode == X_E_TIMES_R) p.e = rsfde_ecoef_at(c, a.m);
     p.spec.kind = a.spec;
     if (last) {
       p.Y = (a.spectral && d > 1) ? c->W[buf] : out;
@@ -293,12 +303,13 @@ static rsfde_status oper_chain(rsfde_ctx* c, const ChainArgs& a, double* out, cu
     }
   }
   if (a.spectral && d > 1) {
-    // inverse DSTs along axes d-2 .. 0
+    // inverse DSTs along the other axes (chain order reversed)
     const double* in = c->W[buf];
-    for (int ax = d - 2; ax >= 0; --ax) {
+    for (int k = d - 2; k >= 0; --k) {
+      const int ax = ord[k];
       PassParams p = rsfde_axis_params(c, ax);
       p.X = in;
-      double* o = ax == 0 ? out : c->W[(buf + 1) % 4];
+      double* o = k == 0 ? out : c->W[(buf + 1) % 4];
       p.Y = o;
       LAUNCH(PC_DST, 16.0 * (double)c->geo.NP, launch_dst_pass(p, false, s), "dst pass");
       in = o;
