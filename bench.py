@@ -273,8 +273,10 @@ def run_ours(args):
     for i in range(args.warmup):
         step(i, u)
     torch.cuda.synchronize()
-    # ---------------- device-timed region (inputs resident in HBM; vectors > L2)
-    S.profile(True)
+    # ---------------- device-timed region (inputs resident in HBM; vectors > L2).  The library's
+    # per-launch profiling events are off here (they cost a few microseconds per launch, which matters
+    # for the launch-bound C1/C2); the same K steps are then re-run with them on for the roofline and
+    # the kernel breakdown (second timed region, also CUDA events on the launching stream).
     S.launch_count(reset=True)
     clocks = ClockSampler(local)
     barrier(ws)
@@ -290,9 +292,19 @@ def run_ours(args):
     barrier(ws)
     clk = clocks.stop()
     launches = S.launch_count(reset=True)
+    t_dev = e0.elapsed_time(e1) * 1e-3
+    # profiled re-run of the same steps (roofline / breakdown)
+    S.profile(True)
+    torch.cuda.synchronize()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for i in range(args.warmup, args.warmup + args.steps):
+        step(i, u)
+    p1.record(stream)
+    torch.cuda.synchronize()
     prof = S.profile_read()
     S.profile(False)
-    t_dev = e0.elapsed_time(e1) * 1e-3
+    t_prof = p0.elapsed_time(p1) * 1e-3
     t_max = max_over_ranks(t_dev, ws, dev)
     unk_its = sum_over_ranks(float(N * sum(iters)), ws, dev)
     value = unk_its / t_max
@@ -358,6 +370,7 @@ def run_ours(args):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * t_max / args.steps, "seconds_per_cn_step": t_max / args.steps,
+        "profiled_ms_per_step": 1e3 * t_prof / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload), "n": list(prob.n),
