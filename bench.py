@@ -270,13 +270,32 @@ def run_ours(args):
             raise RuntimeError(f"GMRES did not converge at step m={m}: {rep}")
         return rep["iters"][0]
 
-    for i in range(args.warmup):
-        step(i, u)
+    Fstack = Fs[0] if prob.source_static else torch.stack(Fs)
+
+    def march(uu, K):
+        """K CN steps from psi through the march API (one rsfde_solve_steps call per <= M steps; the
+        state is reset to psi between calls when K > M).  The caller resets uu to psi beforehand."""
+        its, k = [], 0
+        while k < K:
+            cnt = min(K - k, prob.M)
+            if k > 0:
+                uu.copy_(u0)
+            F = Fstack if prob.source_static else Fstack[:cnt]
+            rep = S.solve_steps(uu, F=F, F_static=bool(prob.source_static), m_begin=0, m_count=cnt, cfg=cfg)
+            if not all(rep["converged"]):
+                raise RuntimeError(f"GMRES did not converge: {rep}")
+            its += rep["iters"]
+            k += cnt
+        return its
+
+    u.copy_(u0)
+    march(u, args.warmup)
     torch.cuda.synchronize()
     # ---------------- device-timed region (inputs resident in HBM; vectors > L2).  The library's
     # per-launch profiling events are off here (they cost a few microseconds per launch, which matters
     # for the launch-bound C1/C2); the same K steps are then re-run with them on for the roofline and
     # the kernel breakdown (second timed region, also CUDA events on the launching stream).
+    u.copy_(u0)
     S.launch_count(reset=True)
     clocks = ClockSampler(local)
     barrier(ws)
@@ -284,9 +303,7 @@ def run_ours(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    iters = []
-    for i in range(args.warmup, args.warmup + args.steps):
-        iters.append(step(i, u))
+    iters = march(u, args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(ws)
@@ -294,12 +311,12 @@ def run_ours(args):
     launches = S.launch_count(reset=True)
     t_dev = e0.elapsed_time(e1) * 1e-3
     # profiled re-run of the same steps (roofline / breakdown)
+    u.copy_(u0)
     S.profile(True)
     torch.cuda.synchronize()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
-    for i in range(args.warmup, args.warmup + args.steps):
-        step(i, u)
+    march(u, args.steps)
     p1.record(stream)
     torch.cuda.synchronize()
     prof = S.profile_read()

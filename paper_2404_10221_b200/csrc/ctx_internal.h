@@ -16,6 +16,13 @@ using rsfde::GmresState;
 
 struct rsfde_ctx {
   int device = 0;  // CUDA device the context lives on (set by setup)
+  // on-chip 1-D march (lazily allocated): generator table, per-step outputs, device copy of host F
+  double* d_s0 = nullptr;
+  int* d_on_iters = nullptr;
+  double* d_on_relres = nullptr;
+  unsigned char* d_on_conv = nullptr;
+  double* d_on_F = nullptr;
+  long long on_F_cap = 0;
   int d = 0;
   int n[3] = {1, 1, 1};
   double alpha[3] = {2, 2, 2}, kappa[3] = {0, 0, 0};

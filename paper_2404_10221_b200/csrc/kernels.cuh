@@ -43,6 +43,23 @@ struct Spec {
 // first-axis source of the "X" channel of an operator pass
 enum XMode { X_INPUT = 0, X_E_TIMES_R = 1, X_ZERO = 2 };
 
+// on-chip 1-D march (onchip_1d.cu): every CN step and GMRES solve in one CTA
+struct OnchipParams {
+  int n, restart, max_iters, m_begin, m_count;
+  double tol, alpha, eta, tau, ebar;
+  const double *s, *lamH, *q;          // FCD generator s_k, lambda^H_k, tau eigenvalues q_k (device, n)
+  const double *a_half, *b_half;       // e = a(t) + b(t) g(x) + k(x) at the half levels (device, M)
+  const double *g, *kk;                // axis factors (device, n) or null
+  const double* F;                     // device, m_count vectors of n (F_stride = n) or one (F_stride = 0); may be null
+  long long F_stride;
+  double* X;                           // u^(m_begin) in, u^(m_begin+m_count) out (device, n)
+  int* iters;                          // per-step outputs (device, m_count)
+  double* relres;
+  unsigned char* conv;
+};
+size_t onchip_smem_bytes(int n, int restart);
+cudaError_t launch_onchip_1d(const OnchipParams& p, cudaStream_t s);
+
 struct PassParams {
   Geom geo;
   int axis;              // 0-based

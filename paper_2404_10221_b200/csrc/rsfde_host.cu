@@ -525,6 +525,85 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
   return RSFDE_OK;
 }
 
+// ------------------------------------------------------------------------------ on-chip 1-D march
+static bool onchip_eligible(const rsfde_ctx* c, const rsfde_gmres_cfg* cfg) {
+  const char* off = getenv("RSFDE_NO_ONCHIP");
+  if (off && *off && strcmp(off, "0")) return false;
+  if (c->d != 1 || c->ekind != RSFDE_COEF_SEPARABLE) return false;
+  if (cfg->form != RSFDE_FORM_A || cfg->x0_policy != RSFDE_X0_PREV || cfg->fixed_iters > 0) return false;
+  if (cfg->restart < 1 || cfg->restart > 50) return false;
+  return onchip_smem_bytes(c->n[0], cfg->restart) <= 200 * 1024;
+}
+
+static rsfde_status onchip_march(rsfde_ctx* c, int m_begin, int m_count, const double* F, int F_static, bool f_host,
+                                 const rsfde_gmres_cfg& cfg, cudaStream_t s, rsfde_report* rep, long long* total) {
+  const int n = c->n[0];
+  if (!c->d_s0) {
+    CK(cudaMalloc(&c->d_s0, n * sizeof(double)), "alloc");
+    c->allocs.push_back(c->d_s0);
+    CK(cudaMemcpy(c->d_s0, c->s_tab[0].data(), n * sizeof(double), cudaMemcpyHostToDevice), "upload s");
+    CK(cudaMalloc(&c->d_on_iters, c->M * sizeof(int)), "alloc");
+    CK(cudaMalloc(&c->d_on_relres, c->M * sizeof(double)), "alloc");
+    CK(cudaMalloc(&c->d_on_conv, c->M), "alloc");
+    c->allocs.push_back(c->d_on_iters);
+    c->allocs.push_back(c->d_on_relres);
+    c->allocs.push_back(c->d_on_conv);
+  }
+  const double* Fd = F;
+  const long long nF = F ? (F_static ? 1 : m_count) : 0;
+  if (F && f_host) {
+    if (c->on_F_cap < nF * n) {
+      if (c->d_on_F) cudaFree(c->d_on_F);
+      CK(cudaMalloc(&c->d_on_F, nF * n * sizeof(double)), "alloc F");
+      c->on_F_cap = nF * n;
+    }
+    CK(cudaMemcpyAsync(c->d_on_F, F, nF * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D F");
+    Fd = c->d_on_F;
+  }
+  OnchipParams p;
+  p.n = n;
+  p.restart = cfg.restart;
+  p.max_iters = cfg.max_iters > 0 ? cfg.max_iters : 10 * cfg.restart;
+  p.m_begin = m_begin;
+  p.m_count = m_count;
+  p.tol = cfg.tol;
+  p.alpha = c->alpha[0];
+  p.eta = c->eta[0];
+  p.tau = c->tau;
+  p.ebar = c->ebar;
+  p.s = c->d_s0;
+  p.lamH = c->d_lamH[0];
+  p.q = c->d_q[0];
+  p.a_half = c->d_ahalf;
+  p.b_half = c->d_bhalf;
+  p.g = c->d_g[0];
+  p.kk = c->d_k[0];
+  p.F = Fd;
+  p.F_stride = F_static ? 0 : n;
+  p.X = c->X;
+  p.iters = c->d_on_iters;
+  p.relres = c->d_on_relres;
+  p.conv = c->d_on_conv;
+  LAUNCH(PC_OPER_SPEC, 0.0, launch_onchip_1d(p, s), "on-chip march");
+  std::vector<int> its(m_count);
+  std::vector<double> rr(m_count);
+  std::vector<unsigned char> cv(m_count);
+  CK(cudaMemcpyAsync(its.data(), c->d_on_iters, m_count * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(rr.data(), c->d_on_relres, m_count * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaMemcpyAsync(cv.data(), c->d_on_conv, m_count, cudaMemcpyDeviceToHost, s), "D2H");
+  CK(cudaStreamSynchronize(s), "stream sync");
+  *total = 0;
+  for (int k = 0; k < m_count; ++k) {
+    if (its[k] > 0) *total += its[k];
+    if (rep) {
+      if (rep->iters) rep->iters[k] = its[k];
+      if (rep->final_relres) rep->final_relres[k] = rr[k];
+      if (rep->converged) rep->converged[k] = cv[k];
+    }
+  }
+  return RSFDE_OK;
+}
+
 // ------------------------------------------------------------------------------ ABI
 extern "C" {
 
@@ -569,6 +648,7 @@ void rsfde_destroy(rsfde_ctx* c) {
   if (!c) return;
   cudaDeviceSynchronize();
   for (void* p : c->allocs) cudaFree(p);
+  if (c->d_on_F) cudaFree(c->d_on_F);
   if (c->h_flags) cudaFreeHost(c->h_flags);
   prof_collect(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
@@ -855,9 +935,16 @@ rsfde_status rsfde_solve_steps(rsfde_ctx* c, int m_begin, int m_count, double* u
     CKL(launch_axpby(0.0, c->FH, c->tau, c->FH, c->geo.NP, s), "scale");
     return RSFDE_OK;
   };
-  if (!F || F_static) TRY(prepare_F(F));
   long long total = 0;
   bool stopped = false;
+  // small 1-D problems: the whole march in one on-chip kernel (no host round trip per iteration)
+  const bool onchip = onchip_eligible(c, cfg) && m_count > 0;
+  if (onchip) {
+    TRY(onchip_march(c, m_begin, m_count, F, F_static, f_host, *cfg, s, rep, &total));
+    m_count = 0;  // skip the generic loop below
+  } else if (!F || F_static) {
+    TRY(prepare_F(F));
+  }
   for (int k = 0; k < m_count; ++k) {
     const int m = m_begin + k;
     if (stopped) {

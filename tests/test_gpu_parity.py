@@ -325,3 +325,21 @@ def test_batched_march_rejects_duplicate_contexts():
     S = _solver(p)
     with pytest.raises(Exception):
         SV.solve_steps_batch([S, S], [_dev(p.psi_interior()), _dev(p.psi_interior())])
+
+
+# ----------------------------------------------------------------------- on-chip 1-D march
+@pytest.mark.parametrize("restart", [50, 3])
+def test_onchip_1d_march_matches_oracle_and_generic_path(restart, monkeypatch):
+    # small 1-D problems march in one on-chip kernel (onchip_1d.cu); restart = 3 forces GMRES restarts
+    prob = I.config_c1(n=127, M=12)
+    u_on, rep_on = _march(prob, restart=restart)
+    monkeypatch.setenv("RSFDE_NO_ONCHIP", "1")
+    u_gen, rep_gen = _march(prob, restart=restart)
+    monkeypatch.delenv("RSFDE_NO_ONCHIP")
+    assert all(rep_on["converged"]) and all(rep_gen["converged"])
+    assert max(abs(a - b) for a, b in zip(rep_on["iters"], rep_gen["iters"])) <= 1
+    uo, ro, _ = scheme.solve(prob, restart=restart)
+    assert max(abs(a - b) for a, b in zip(rep_on["iters"], ro.iters)) <= 1, (rep_on["iters"], ro.iters)
+    if rep_on["iters"] != ro.iters:
+        uo, ro, _ = scheme.solve(prob, restart=restart, fixed_iters=rep_on["iters"])
+    assert relerr(u_on, uo) < 1e-9
