@@ -1,24 +1,30 @@
 // instantiation of the pencil-pass kernels for FFT length L = 1024 (n = 511, the C5 grid), with the
 // warp-specialised tile pipeline (tile_kernels.cuh) for the spectral operator and DST passes
 #include "tile_kernels.cuh"
+#include <cstdlib>
+#include <cstring>
 namespace rsfde {
 using T1024 = Lay2<32, 32>;
 RSFDE_INSTANTIATE_T(T1024)
 
-// tile width: 128-byte rows where rows are >= 2 MB apart, else 64-byte rows (two CTAs per SM);
-// 0 = no tile pipeline (a strided tile must be adjacent pencils of one block)
+// tile width in pencil pairs: 8 = 128-byte rows (one CTA of 8 compute warps per SM), 4 = 64-byte rows
+// (two CTAs of 4 compute warps per SM), 0 = no tile pipeline (a strided tile must be adjacent pencils
+// of one block)
 static int tile_pairs(const PassParams& p) {
   if (p.flags & PASS_FLAG_NO_PIPE) return 0;
   if (p.contiguous) return 4;
-  // (128-byte rows, TP = 8, measured no faster on the 2 MB-stride axis inside the full pass: the
-  //  FFT work, not the row-piece count, sets the pace there)
+  // 128-byte rows where rows are >= 1 MB apart (x1 of the C5 grid: every row piece is its own 2 MB
+  // page and the TMA rate follows the row-piece count; measured 2 % faster K chain).
+  // RSFDE_TILE128=1 forces them on every eligible strided pass (test coverage at small sizes).
+  const char* f128 = getenv("RSFDE_TILE128");
+  const bool force128 = f128 && strcmp(f128, "0");
+  if (p.inner % 16 == 0 && (force128 || p.stride * 8 >= (1ll << 20))) return 8;
   return p.inner % 8 == 0 ? 4 : 0;
 }
 
 template <int MODE>
 static cudaError_t launch_tile_any(const PassParams& p, int tp, cudaStream_t s) {
-  (void)tp;  // only 64-byte tiles are instantiated (see tile_pairs)
-  return launch_tile<MODE, 4>(p, s);
+  return tp == 8 ? launch_tile<MODE, 8>(p, s) : launch_tile<MODE, 4>(p, s);
 }
 
 cudaError_t launch_oper_1024(const PassParams& p, bool spectral, bool last, cudaStream_t s) {

@@ -343,3 +343,11 @@ def test_onchip_1d_march_matches_oracle_and_generic_path(restart, monkeypatch):
     if rep_on["iters"] != ro.iters:
         uo, ro, _ = scheme.solve(prob, restart=restart, fixed_iters=rep_on["iters"])
     assert relerr(u_on, uo) < 1e-9
+
+
+@pytest.mark.parametrize("kind,shape", [("c5", (511, 15, 31)), ("c5", (15, 511, 31)), ("c5", (511, 511))])
+def test_tile128_matvec_and_precond_parity(kind, shape, monkeypatch, cache):
+    # 128-byte tiles (8 pairs per CTA) serve the 2 MB-stride axis of C5; force them at small sizes
+    monkeypatch.setenv("RSFDE_TILE128", "1")
+    test_matvec_parity(cache, kind, shape, 0)
+    test_precond_parity(cache, kind, shape)
