@@ -24,7 +24,7 @@ static int tile_pairs(const PassParams& p) {
 
 template <int MODE>
 static cudaError_t launch_tile_any(const PassParams& p, int tp, cudaStream_t s) {
-  return tp == 8 ? launch_tile<MODE, 8>(p, s) : launch_tile<MODE, 4>(p, s);
+  return tp == 8 ? launch_tile<MODE, T1024, 8>(p, s) : launch_tile<MODE, T1024, 4>(p, s);
 }
 
 cudaError_t launch_oper_1024(const PassParams& p, bool spectral, bool last, cudaStream_t s) {

@@ -5,6 +5,8 @@ namespace rsfde {
 
 cudaError_t launch_oper_1024(const PassParams& p, bool spectral, bool last, cudaStream_t s);
 cudaError_t launch_dst_1024(const PassParams& p, bool last, cudaStream_t s);
+cudaError_t launch_oper_512(const PassParams& p, bool spectral, bool last, cudaStream_t s);
+cudaError_t launch_dst_512(const PassParams& p, bool last, cudaStream_t s);
 extern template cudaError_t launch_oper_t<Lay2<2, 2>>(const PassParams&, bool, bool, cudaStream_t);
 extern template cudaError_t launch_dst_t<Lay2<2, 2>>(const PassParams&, bool, cudaStream_t);
 extern template cudaError_t launch_oper_t<Lay2<4, 2>>(const PassParams&, bool, bool, cudaStream_t);
@@ -37,7 +39,7 @@ cudaError_t launch_oper_pass(const PassParams& p, bool spectral, bool last, cuda
     case 64: return launch_oper_t<Lay2<32, 2>>(p, spectral, last, s);
     case 128: return launch_oper_t<Lay2<32, 4>>(p, spectral, last, s);
     case 256: return launch_oper_t<Lay2<32, 8>>(p, spectral, last, s);
-    case 512: return launch_oper_t<Lay2<32, 16>>(p, spectral, last, s);
+    case 512: return launch_oper_512(p, spectral, last, s);
     case 1024: return launch_oper_1024(p, spectral, last, s);
     case 2048: return launch_oper_t<Lay3<2>>(p, spectral, last, s);
     case 4096: return launch_oper_t<Lay3<4>>(p, spectral, last, s);
@@ -54,7 +56,7 @@ cudaError_t launch_dst_pass(const PassParams& p, bool last, cudaStream_t s) {
     case 64: return launch_dst_t<Lay2<32, 2>>(p, last, s);
     case 128: return launch_dst_t<Lay2<32, 4>>(p, last, s);
     case 256: return launch_dst_t<Lay2<32, 8>>(p, last, s);
-    case 512: return launch_dst_t<Lay2<32, 16>>(p, last, s);
+    case 512: return launch_dst_512(p, last, s);
     case 1024: return launch_dst_1024(p, last, s);
     case 2048: return launch_dst_t<Lay3<2>>(p, last, s);
     case 4096: return launch_dst_t<Lay3<4>>(p, last, s);

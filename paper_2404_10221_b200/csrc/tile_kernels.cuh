@@ -46,25 +46,26 @@ __device__ int g_trace_launch = 0, g_trace_target = -1;  // launch counter / lau
 #define TTRACE(slot)
 #endif
 
-// Tile width TP pencil pairs (one compute warp each): TP = 8 -> 16 pencils = 128-byte rows, one CTA
-// of 12 warps per SM; TP = 4 -> 64-byte rows, two CTAs of 8 warps per SM.  128-byte rows are
-// needed on axes whose rows are >= 2 MB apart (every row piece is then its own 2 MB page, and TMA
-// throughput is set by the number of row pieces: tools/micro/tma_micro.cu, 3.0 vs 5.9 TB/s).
-template <int TP>
+// Tile width TP pencil pairs.  A pair is one FFT group of T::G threads (32 at L = 1024, 16 at
+// L = 512), so a compute warp holds 32 / G pairs and a tile CW = TP G / 32 compute warps.  CW = 8: one
+// CTA of 12 warps per SM (compute warps at 232 registers); CW = 4: two CTAs of 8 warps per SM (216).
+// 128-byte rows (TP = 8) are needed on axes whose rows are >= 1 MB apart (every row piece is then its
+// own 2 MB page, and TMA throughput is set by the number of row pieces: tools/micro/tma_micro.cu,
+// 3.0 vs 5.9 TB/s).
+template <int CW>
 struct TileCfg {
-  static constexpr int kTilePencils = 2 * TP;                       // adjacent pencils per tile
-  static constexpr int kRowBytes = 8 * kTilePencils;                // bytes of one tile row
-  static constexpr int kTileThreads = TP == 8 ? 384 : 256;
-  static constexpr int kCtasPerSm = TP == 8 ? 1 : 2;
-  static constexpr int kComputeRegs = TP == 8 ? 232 : 216;
+  static constexpr int kTileThreads = CW == 8 ? 384 : 256;
+  static constexpr int kCtasPerSm = CW == 8 ? 1 : 2;
+  static constexpr int kComputeRegs = CW == 8 ? 232 : 216;
 };
 constexpr int kProducerRegs = 40;
 constexpr int kBoxRows = 256;
-#define RSFDE_TILE_CONSTS                                              \
-  constexpr int kTilePairs = TP;                                       \
-  constexpr int kTilePencils = TileCfg<TP>::kTilePencils;              \
-  constexpr int kRowBytes = TileCfg<TP>::kRowBytes;                    \
-  constexpr size_t kStageBytes = 2 * (size_t)kBoxRows * kRowBytes;     \
+#define RSFDE_TILE_CONSTS                                                        \
+  constexpr int kTilePairs = TP;                                                 \
+  constexpr int kTilePencils = 2 * TP;                   /* adjacent pencils */  \
+  constexpr int kRowBytes = 8 * kTilePencils;            /* bytes of a row */    \
+  constexpr int kNBox = NH / kBoxRows;                   /* boxes per job */     \
+  constexpr size_t kStageBytes = (size_t)kNBox * kBoxRows * kRowBytes;           \
   (void)kTilePairs; (void)kTilePencils; (void)kRowBytes; (void)kStageBytes;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -97,11 +98,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-template <int TP>
-__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * TP) : "memory"); }
+template <int CW>
+__device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * CW) : "memory"); }
 
 // element offset of the first pencil of tile t (strided: pencil 16t; contiguous: row 16t)
-template <int TP, bool CT>
+template <int TP, int NH, bool CT>
 __device__ __forceinline__ long long tile_base(const PassParams& p, long long t) {
   RSFDE_TILE_CONSTS
   if (CT) return kTilePencils * t * p.geo.P;
@@ -125,19 +126,20 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, in
 // Contiguous axis: tensor map {P, rows}, box {256, 16} -> stage[half][row][256].
 
 // producer: one lane streams one tile input into the stage (two box copies)
-template <int TP, bool CT>
+template <int TP, int NH, bool CT>
 __device__ __forceinline__ void produce(const PassParams& p, const CUtensorMap* tm, long long t, char* stage,
                                         unsigned long long* full) {
   RSFDE_TILE_CONSTS
   mbar_expect_tx(full, (unsigned)kStageBytes);
   if (CT) {
-    tma_load_3d(stage, tm, 0, (int)(kTilePencils * t), 0, full);
-    tma_load_3d(stage + kStageBytes / 2, tm, kBoxRows, (int)(kTilePencils * t), 0, full);
+#pragma unroll
+    for (int b = 0; b < kNBox; ++b)
+      tma_load_3d(stage + (size_t)b * (kStageBytes / kNBox), tm, b * kBoxRows, (int)(kTilePencils * t), 0, full);
   } else {
     const unsigned pen = (unsigned)(kTilePencils * t), inner = (unsigned)p.inner;
     const int o = (int)(pen / inner), i = (int)(pen - (unsigned)o * inner);
-    tma_load_3d(stage, tm, i, 0, o, full);
-    tma_load_3d(stage + kStageBytes / 2, tm, i, kBoxRows, o, full);
+#pragma unroll
+    for (int b = 0; b < kNBox; ++b) tma_load_3d(stage + (size_t)b * (kStageBytes / kNBox), tm, i, b * kBoxRows, o, full);
   }
 }
 
@@ -152,7 +154,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // value pair (p, q) of compute warp w at axis position j (1..n) from the stage
-template <int TP, bool CT>
+template <int TP, int NH, bool CT>
 __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* stage, int w, int j) {
   RSFDE_TILE_CONSTS
   const int r = j - 1;
@@ -169,40 +171,42 @@ __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* s
 // conflict-free across the 8 buffers
 __device__ __forceinline__ int oswz(int k, int w) { return k ^ (w & 7); }
 
-template <int MODE, int TP, bool CT>
-__global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasPerSm) tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR,
-                                                          const __grid_constant__ CUtensorMap tmX) {
+template <int MODE, class T, int TP, bool CT>
+__global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg<TP * T::G / 32>::kCtasPerSm)
+    tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmX) {
+  constexpr int E = T::E, G = T::G, L = T::L, N = T::N, NH = T::N;
+  constexpr int PPW = 32 / G;           // pencil pairs per compute warp
+  constexpr int CW = TP / PPW;          // compute warps
+  constexpr int kComputeThreads = 32 * CW;
   RSFDE_TILE_CONSTS
-  using T = Lay2<32, 32>;
-  constexpr int E = 32, G = 32, L = 1024, N = 512;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
   constexpr bool LAST = MODE == MODE_OPER_SPEC_LAST || MODE == MODE_DST_LAST;
   extern __shared__ __align__(128) char tsm_raw[];
   char* tsm = tsm_raw + ((1024u - (smem_u32(tsm_raw) & 1023u)) & 1023u);  // TMA swizzle needs 1 KB alignment
-  double2* bufs = reinterpret_cast<double2*>(tsm);                        // 8 x 16 KB
+  double2* bufs = reinterpret_cast<double2*>(tsm);                        // TP x L x 16 bytes
   char* stage = tsm + (size_t)kTilePairs * L * sizeof(double2);           // 1024-aligned
   __shared__ __align__(8) unsigned long long full_bar, empty_bar;
-  __shared__ int tvalid[kTilePairs];  // validity bits (p, q) of each warp's pair in the current tile
+  __shared__ int tvalid[kTilePairs];  // validity bits (p, q) of each pair in the current tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long ntiles = CT ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
   const int jobs_per_tile = OPER ? (p.xmode == X_ZERO ? 1 : 2) : 1;
   if (threadIdx.x == 0) {
     mbar_init(&full_bar, 1);
-    mbar_init(&empty_bar, kTilePairs);
+    mbar_init(&empty_bar, CW);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  if (warp >= kTilePairs) {
+  if (warp >= CW) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    if (warp != kTilePairs) return;
+    if (warp != CW) return;
     // ------------------------------------------------------------------ producer warp
     long long job = 0;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
       for (int k = 0; k < jobs_per_tile; ++k, ++job) {
         if (job > 0) mbar_wait(&empty_bar, (unsigned)((job - 1) & 1));
         const CUtensorMap* src = OPER ? ((k == 0 || p.xmode == X_E_TIMES_R) ? &tmR : &tmX) : &tmX;
-        if (lane == 0) produce<TP, CT>(p, src, t, stage, &full_bar);
+        if (lane == 0) produce<TP, NH, CT>(p, src, t, stage, &full_bar);
         __syncwarp();
       }
     }
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
   }
 
   // -------------------------------------------------------------------- compute warps
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(TileCfg<TP>::kComputeRegs));
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(TileCfg<CW>::kComputeRegs));
   // separable e(x, t) along the pass axis (X = E o R): the axis factors g_a, k_a in shared memory
   // (last axis: the same arrays hold the spectrum tables lambda^H_k and tq_k of the axis)
   __shared__ double e_ga[N], e_ka[N];
@@ -218,22 +222,22 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
   if (e_tab) {
     const double* ga = p.e.g[p.axis];
     const double* ka = p.e.k[p.axis];
-    for (int j = threadIdx.x; j < N; j += 32 * kTilePairs) {
+    for (int j = threadIdx.x; j < N; j += kComputeThreads) {
       e_ga[j] = (ga && j < p.n) ? __ldg(ga + j) : 1.0;
       e_ka[j] = (ka && j < p.n) ? __ldg(ka + j) : 0.0;
     }
-    compute_bar<TP>();
+    compute_bar<CW>();
   }
   if (LAST && !e_tab) {
     const double* lh = p.spec.lamH[p.axis];
     const double* tq = p.spec.tq[p.axis];
-    for (int j = threadIdx.x; j < N; j += 32 * kTilePairs) {
+    for (int j = threadIdx.x; j < N; j += kComputeThreads) {
       e_ga[j] = (lh && j < p.n) ? __ldg(lh + j) : 1.0;
       e_ka[j] = (tq && j < p.n) ? __ldg(tq + j) : 0.0;
     }
-    compute_bar<TP>();
+    compute_bar<CW>();
   }
-  const int w = warp, g = lane;
+  const int g = lane % G, w = warp * PPW + lane / G;  // FFT-group thread index, pencil pair in the tile
   double2* buf = bufs + w * L;
   const double rs = p.rscale ? __ldg(p.rscale) : 1.0;
   const double hs = 0.5 * p.dst_scale;
@@ -247,7 +251,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
     const long long pair = (long long)kTilePairs * t + w;
     const bool active = pair < p.npairs;
     const PairCtx pc = make_pair(p, active ? pair : 0, active);
-    if (lane == 0) tvalid[w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
+    if (g == 0) tvalid[w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
     double2 v[E];
     TTRACE(0)
     // ---- job 0: primary input
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
         if (m < E / 2 && j >= 1 && j <= p.n) {
-          r = stage_pair<TP, CT>(p, stage, w, j);
+          r = stage_pair<TP, NH, CT>(p, stage, w, j);
           r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
         }
         v[m] = r;
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
         if (j >= 1 && j <= p.n) {
-          r = stage_pair<TP, CT>(p, stage, w, j);
+          r = stage_pair<TP, NH, CT>(p, stage, w, j);
           r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
         }
         v[m] = r;
@@ -293,11 +297,16 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
       asm volatile("mov.b32 %0, %1;" : "=r"(ph) : "r"(ph0));
       const unsigned long long cmsk = (ph == 1) ? 0x8000000000000000ull : 0ull;
       if (!(RSFDE_TILE_SKIP & 1)) {
+        if constexpr (E == G) {
 #pragma unroll
-        for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
-        fft_fwd<E, G>(v, buf, g, p.tw);
+          for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
+          fft_fwd<E, G>(v, buf, g, p.tw);
 #pragma unroll
-        for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
+          for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
+        } else {
+          (void)cmsk;
+          T::fft(v, buf, g, p.tw, ph == 1);  // E = R G: forward and inverse differ in layout
+        }
       }
       TTRACE(2 + ph)
       if (OPER && ph == 0) {
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
           // store C
           if (CT) {
             __syncwarp();
-            for (int j = g + 1; j <= p.n; j += 32) {
+            for (int j = g + 1; j <= p.n; j += G) {
               const double2 c = buf[oswz(j, w)];
               if (RSFDE_TILE_SKIP & 2) continue;
               if (pc.vp) p.C[pc.off_p + j - 1] = c.x;
@@ -333,9 +342,9 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
             }
             __syncwarp();
           } else {
-            compute_bar<TP>();
-            const long long base = tile_base<TP, CT>(p, t);
-            for (int e = threadIdx.x; e < p.n * kTilePairs; e += 32 * kTilePairs) {
+            compute_bar<CW>();
+            const long long base = tile_base<TP, NH, CT>(p, t);
+            for (int e = threadIdx.x; e < p.n * kTilePairs; e += kComputeThreads) {
               const int row = e / kTilePairs, q = e % kTilePairs;
               const double2 c = bufs[q * L + oswz(row + 1, q)];
               const int vm = tvalid[q];
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
               if (vm & 2) *reinterpret_cast<double2*>(dst) = c;
               else *dst = c.x;
             }
-            compute_bar<TP>();
+            compute_bar<CW>();
           }
         }
         TTRACE(9)
@@ -363,7 +372,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
           const int j = g + G * m;
           double2 x = make_double2(0.0, 0.0);
           if (p.xmode != X_ZERO && j >= 1 && j <= p.n) {
-            x = stage_pair<TP, CT>(p, stage, w, j);
+            x = stage_pair<TP, NH, CT>(p, stage, w, j);
             if (p.xmode == X_E_TIMES_R) {
               double2 e;
               if (e_tab) {
@@ -411,6 +420,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
           if (!T::lower(r)) continue;
           buf[T::rowk(g, r)] = make_double2(-v[r].y * hs, v[r].x * hs);
         }
+        __syncwarp();  // (E > G: the loop below reads k values written by other threads of the group)
         // Lambda = (ebar + cP + tq_k) cH lh_k (P_hat) | (ebar + cP + tq_k) (P_alpha) | cH lh_k (H):
         // one fast reciprocal per value instead of an IEEE division
         const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
@@ -472,7 +482,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
         }
         if (CT) {
           __syncwarp();
-          for (int j = g + 1; j <= p.n; j += 32) {
+          for (int j = g + 1; j <= p.n; j += G) {
             const double2 yv = buf[oswz(j, w)];
             if (RSFDE_TILE_SKIP & 2) continue;
             if (pc.vp) p.Y[pc.off_p + j - 1] = yv.x;
@@ -480,9 +490,9 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
           }
           __syncwarp();
         } else {
-          compute_bar<TP>();
-          const long long base = tile_base<TP, CT>(p, t);
-          for (int e = threadIdx.x; e < p.n * kTilePairs; e += 32 * kTilePairs) {
+          compute_bar<CW>();
+          const long long base = tile_base<TP, NH, CT>(p, t);
+          for (int e = threadIdx.x; e < p.n * kTilePairs; e += kComputeThreads) {
             const int row = e / kTilePairs, q = e % kTilePairs;
             const int vm = tvalid[q];
             if (!(vm & 1)) continue;
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
               if (vm & 2) *reinterpret_cast<double2*>(dst) = yv;
             else *dst = yv.x;
           }
-          compute_bar<TP>();
+          compute_bar<CW>();
         }
       }
     }
@@ -502,13 +512,13 @@ __global__ void __launch_bounds__(TileCfg<TP>::kTileThreads, TileCfg<TP>::kCtasP
   // count launches (the last compute thread to finish bumps the counter once per launch)
   __shared__ int done_warps;
   if (threadIdx.x == 0) done_warps = 0;
-  compute_bar<TP>();
+  compute_bar<CW>();
   if (lane == 0 && atomicAdd(&done_warps, 1) == 0 && blockIdx.x == 0) atomicAdd(&g_trace_launch, 1);
 #endif
 }
 
 // host: tensor map of one input vector for this pass (see the stage layout above)
-template <int TP>
+template <int TP, int NH>
 static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtensorMap* tm) {
   RSFDE_TILE_CONSTS
   // driver entry point, fetched once (thread-safe static initialisation)
@@ -541,15 +551,16 @@ static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtenso
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <int MODE, int TP, bool CT>
+template <int MODE, class T, int TP, bool CT>
 cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
+  constexpr int NH = T::N, CW = TP * T::G / 32;
   RSFDE_TILE_CONSTS
-  constexpr int kTileThreads = TileCfg<TP>::kTileThreads, kCtasPerSm = TileCfg<TP>::kCtasPerSm;
+  constexpr int kTileThreads = TileCfg<CW>::kTileThreads, kCtasPerSm = TileCfg<CW>::kCtasPerSm;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
-  const size_t smem = (size_t)kTilePairs * 1024 * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
+  const size_t smem = (size_t)kTilePairs * T::L * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
   // kernel attribute and SM count, once per process (thread-safe static initialisation)
   static const int sms = [smem]() -> int {
-    if (cudaFuncSetAttribute(tile_kernel<MODE, TP, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+    if (cudaFuncSetAttribute(tile_kernel<MODE, T, TP, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return -1;
     int dev = 0, n = 0;
@@ -562,16 +573,16 @@ cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
   memset(&tmR, 0, sizeof(tmR));
   memset(&tmX, 0, sizeof(tmX));
   cudaError_t err = cudaSuccess;
-  if (OPER) err = tile_tensor_map<TP>(p, p.R, &tmR);
-  if (err == cudaSuccess && (!OPER || p.xmode == X_INPUT)) err = tile_tensor_map<TP>(p, p.X, &tmX);
+  if (OPER) err = tile_tensor_map<TP, NH>(p, p.R, &tmR);
+  if (err == cudaSuccess && (!OPER || p.xmode == X_INPUT)) err = tile_tensor_map<TP, NH>(p, p.X, &tmX);
   if (err != cudaSuccess) return err;
   const long long ntiles = p.contiguous ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
   const long long blocks = ntiles < (long long)kCtasPerSm * sms ? ntiles : (long long)kCtasPerSm * sms;
-  tile_kernel<MODE, TP, CT><<<(unsigned)blocks, kTileThreads, smem, s>>>(p, tmR, tmX);
+  tile_kernel<MODE, T, TP, CT><<<(unsigned)blocks, kTileThreads, smem, s>>>(p, tmR, tmX);
   err = cudaGetLastError();
   if (err != cudaSuccess && getenv("RSFDE_DEBUG")) {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, tile_kernel<MODE, TP, CT>);
+    cudaFuncGetAttributes(&a, tile_kernel<MODE, T, TP, CT>);
     fprintf(stderr, "tile_kernel<%d>: regs %d maxthreads %d static %zu maxdyn %d local %zu smem %zu blocks %lld\n", MODE,
             a.numRegs, a.maxThreadsPerBlock, a.sharedSizeBytes, a.maxDynamicSharedSizeBytes, a.localSizeBytes, smem,
             blocks);
@@ -580,9 +591,9 @@ cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
 }
 
 // contiguous (last-axis) and strided tiles are separate kernels (smaller code, fewer branches)
-template <int MODE, int TP>
+template <int MODE, class T, int TP>
 cudaError_t launch_tile(const PassParams& p, cudaStream_t s) {
-  return p.contiguous ? launch_tile_ct<MODE, TP, true>(p, s) : launch_tile_ct<MODE, TP, false>(p, s);
+  return p.contiguous ? launch_tile_ct<MODE, T, TP, true>(p, s) : launch_tile_ct<MODE, T, TP, false>(p, s);
 }
 
 }  // namespace rsfde

@@ -58,7 +58,9 @@ SHAPES = [("c1", (255,)), ("c1", (7,)), ("c1", (1,)), ("c5", (31, 63)), ("c5", (
           ("c5", (2047, 7)), ("c5", (7, 2047)), ("c5", (3, 1023, 3)), ("c1", (2047,)),
           # n = 511 pencils: the warp-specialised tile pipeline (strided tiles of 16 pencils, a
           # ragged last tile, the pad column, and contiguous 16-row tiles)
-          ("c5", (511, 15, 31)), ("c5", (15, 511, 7)), ("c5", (7, 15, 511)), ("c5", (511, 511)), ("c1", (511,))]
+          ("c5", (511, 15, 31)), ("c5", (15, 511, 7)), ("c5", (7, 15, 511)), ("c5", (511, 511)), ("c1", (511,)),
+          # n = 255 pencils: the tile pipeline with two 16-thread FFT groups per warp (L = 512, C4)
+          ("c5", (255, 15, 31)), ("c5", (15, 255, 31)), ("c5", (7, 15, 255)), ("c5", (255, 255))]
 
 
 @pytest.fixture(scope="module")
