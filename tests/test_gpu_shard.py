@@ -27,7 +27,9 @@ def relerr(got, ref):
     return float(np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300))
 
 
-@pytest.mark.parametrize("shape,P", [((15, 7, 31), 2), ((31, 15, 15), 4), ((63, 31, 7), 8), ((63, 63, 63), 4)])
+@pytest.mark.parametrize("shape,P", [((15, 7, 31), 2), ((31, 15, 15), 4), ((63, 31, 7), 8), ((63, 63, 63), 4),
+                                     # n = 511 / 255 axes: the tile pipelines in both slab layouts
+                                     ((511, 15, 31), 2), ((15, 31, 511), 4), ((255, 15, 31), 2), ((31, 15, 255), 2)])
 def test_sharded_operators_match_oracle(shape, P):
     from paper_2404_10221_b200 import _lib as L
     from paper_2404_10221_b200.solver import RsfdeTeam
@@ -46,7 +48,7 @@ def test_sharded_operators_match_oracle(shape, P):
         assert relerr(_host(T.precond(kind, _dev(x))), ref) < 1e-12
 
 
-@pytest.mark.parametrize("shape,P", [((31, 15, 63), 2), ((15, 15, 15), 4), ((63, 63, 31), 8)])
+@pytest.mark.parametrize("shape,P", [((31, 15, 63), 2), ((15, 15, 15), 4), ((63, 63, 31), 8), ((511, 15, 31), 2)])
 def test_sharded_march_matches_oracle_and_single_gpu(shape, P):
     from paper_2404_10221_b200.solver import RsfdeSolver, RsfdeTeam
     prob = I.config_c5(M=3, nn=shape)
