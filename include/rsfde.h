@@ -143,7 +143,11 @@ rsfde_status rsfde_gmres_step(rsfde_ctx *ctx, int m, const double *b, double *x,
    vector (F_static != 0); F == NULL means F = 0.  u and F may be DEVICE or HOST pointers
    (host pointers are staged through device memory inside the call; the copies are timed
    in loop_seconds).  Returns RSFDE_OK also when a step did not converge: the report flags
-   it and the march stops at that step (rep->iters of later steps = -1). */
+   it and the march stops at that step (rep->iters of later steps = -1).
+   Small 1-D problems (d = 1, A form, separable e, x0 = u^(m), no replay, restart <= 50 and the
+   basis within ~200 KB of shared memory) run the whole march in one on-chip kernel (one CTA:
+   no host synchronisation per GMRES iteration); the environment variable RSFDE_NO_ONCHIP=1
+   selects the generic path.  Both follow the same algorithm (results agree to rounding). */
 rsfde_status rsfde_solve_steps(rsfde_ctx *ctx, int m_begin, int m_count, double *u, const double *F, int F_static,
                                const rsfde_gmres_cfg *cfg, rsfde_report *rep, void *stream);
 
