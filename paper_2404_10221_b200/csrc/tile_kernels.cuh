@@ -240,7 +240,11 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   const int g = lane % G, w = warp * PPW + lane / G;  // FFT-group thread index, pencil pair in the tile
   double2* buf = bufs + w * L;
   const double rs = p.rscale ? __ldg(p.rscale) : 1.0;
+  // The DST scale hs is applied once, early: to the input of a DST pass, to y = H X + eta T R in an
+  // operator pass and to Lambda^-1 before the last inverse DST -- never to the row-layout outputs.
   const double hs = 0.5 * p.dst_scale;
+  const double rsh = rs * hs;
+  const double hc0s = p.hc0 * hs, hc1s = p.hc1 * hs, etas = p.eta * hs;
   long long job = 0;
   int tcount = 0;
   (void)tcount;
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         double2 r = make_double2(0.0, 0.0);
         if (j >= 1 && j <= p.n) {
           r = stage_pair<TP, NH, CT>(p, stage, w, j);
-          r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
+          r = make_double2(pc.vp ? rsh * r.x : 0.0, pc.vq ? rsh * r.y : 0.0);
         }
         v[m] = r;
       }
@@ -402,8 +406,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           double2 y = make_double2(0.0, 0.0);
           if (j >= 1 && j <= p.n) {
             const double2 xl = buf[j - 1], x0 = buf[j], xn = buf[j + 1];
-            y.x = fma(p.hc0, x0.x, fma(p.hc1, xl.x + xn.x, p.eta * v[m].x));
-            y.y = fma(p.hc0, x0.y, fma(p.hc1, xl.y + xn.y, p.eta * v[m].y));
+            y.x = fma(hc0s, x0.x, fma(hc1s, xl.x + xn.x, etas * v[m].x));
+            y.y = fma(hc0s, x0.y, fma(hc1s, xl.y + xn.y, etas * v[m].y));
           }
           v[m] = y;
         }
@@ -418,14 +422,14 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
 #pragma unroll
         for (int r = 0; r < E; ++r) {
           if (!T::lower(r)) continue;
-          buf[T::rowk(g, r)] = make_double2(-v[r].y * hs, v[r].x * hs);
+          buf[T::rowk(g, r)] = make_double2(-v[r].y, v[r].x);
         }
         __syncwarp();  // (E > G: the loop below reads k values written by other threads of the group)
         // Lambda = (ebar + cP + tq_k) cH lh_k (P_hat) | (ebar + cP + tq_k) (P_alpha) | cH lh_k (H):
         // one fast reciprocal per value instead of an IEEE division
         const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
-        const double icHp = (S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_p;
-        const double icHq = (S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_q;
+        const double icHp = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_p) * hs;  // (hs of the inverse DST)
+        const double icHq = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_q) * hs;
         if (fast && !e_tab) {
           // unrolled: the 16 values are independent (a rolled loop serialises the latencies)
 #pragma unroll
@@ -454,8 +458,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             if (k >= 1) {
               const double2 z = buf[k];
               const double2 lam = spec_pair(p, kc, k);
-              wv.x = pc.vp ? z.x / lam.x : 0.0;
-              wv.y = pc.vq ? z.y / lam.y : 0.0;
+              wv.x = pc.vp ? (z.x * hs) / lam.x : 0.0;
+              wv.y = pc.vq ? (z.y * hs) / lam.y : 0.0;
             }
             buf[k] = wv;
           }
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
 #pragma unroll
         for (int r = 0; r < E; ++r) {
           if (!T::lower(r)) continue;
-          buf[oswz(T::rowk(g, r), w)] = make_double2(-v[r].y * hs, v[r].x * hs);
+          buf[oswz(T::rowk(g, r), w)] = make_double2(-v[r].y, v[r].x);
         }
         if (CT) {
           __syncwarp();
