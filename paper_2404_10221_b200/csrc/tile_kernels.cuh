@@ -244,7 +244,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   // operator pass and to Lambda^-1 before the last inverse DST -- never to the row-layout outputs.
   const double hs = 0.5 * p.dst_scale;
   const double rsh = rs * hs;
-  const double hc0s = p.hc0 * hs, hc1s = p.hc1 * hs, etas = p.eta * hs;
+  // the lazy basis scale rs of R folds into eta (T R enters y only as eta T R) and into the C factor
+  const double hc0s = p.hc0 * hs, hc1s = p.hc1 * hs, etas = p.eta * rsh, crs = OPER ? rsh : hs;
   long long job = 0;
   int tcount = 0;
   (void)tcount;
@@ -267,8 +268,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
         if (m < E / 2 && j >= 1 && j <= p.n) {
-          r = stage_pair<TP, NH, CT>(p, stage, w, j);
-          r = make_double2(pc.vp ? rs * r.x : 0.0, pc.vq ? rs * r.y : 0.0);
+          r = stage_pair<TP, NH, CT>(p, stage, w, j);  // raw R (rs folded into eta and the C factor)
+          r = make_double2(pc.vp ? r.x : 0.0, pc.vq ? r.y : 0.0);
         }
         v[m] = r;
       }
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             if (!T::lower(r)) continue;
             const int k = T::rowk(g, r);
             const double2 zm = buf[(L - k) & (L - 1)];
-            const double f = (k >= 1) ? hs * __ldg(p.lamH + k - 1) : 0.0;
+            const double f = (k >= 1) ? crs * __ldg(p.lamH + k - 1) : 0.0;
             cv[i++] = make_double2(-(v[r].y - zm.y) * f, (v[r].x - zm.x) * f);
           }
           __syncwarp();
