@@ -1,15 +1,16 @@
-// Warp-specialised tile pipeline for the L = 1024 pencil passes (n = 511: the C5 hot path).
+// Warp-specialised tile pipeline for the spectral operator and DST pencil passes at L = 1024 (n = 511,
+// C5) and L = 512 (n = 255, C4).
 //
-// A CTA (one per SM, persistent) = 8 compute warps + 1 producer warp.  A tile = 8 adjacent pencil
-// pairs: on a strided axis 16 adjacent pencils = 128 contiguous bytes of every row, on the
-// contiguous axis 16 adjacent rows.  The producer streams each tile input into one shared stage with
-// cp.async.bulk (one 128-byte row piece or one 4 KB row per copy) tracked by an mbarrier
-// transaction count; the compute warps read their pair's column out of the stage, release it (so
-// the next input streams in while they compute) and run the FFT phases of pass_kernels.cuh with the
-// same per-pair shared buffers.  Strided outputs go out as 128-byte rows stored cooperatively by
-// the 8 compute warps (measured: 128-byte row tiles move 2.9x faster than one row per lane,
-// tools/micro/pattern_micro.cu).  Neighbouring pairs are processed in lockstep, so every DRAM
-// sector is read and written once (ncu).
+// A persistent CTA = CW compute warps + one producer warpgroup (setmaxnreg moves its registers to the
+// compute warps).  A tile = TP adjacent pencil pairs, one FFT group (G threads) per pair: on a strided
+// axis 2 TP adjacent pencils = 16 TP contiguous bytes of every row, on the contiguous axis 2 TP
+// adjacent rows.  The producer streams each tile input into a shared stage with cp.async.bulk.tensor
+// box loads (tensor maps built per launch on the host) tracked by an mbarrier transaction count; the
+// compute warps read their pair's column out of the swizzled stage, release it (the next input
+// streams in while they compute) and run the FFT phases with per-pair shared exchange buffers.
+// Strided outputs leave as row pieces stored cooperatively by the compute warps; neighbouring pairs
+// are processed in lockstep, so every DRAM sector is read and written once (ncu:
+// profiles/r01_ncu_traffic.json).
 //
 // Job sequence per tile (consumed in the same order by producer and compute warps):
 //   spectral operator pass:  [R_t] [X_t (X_INPUT) | R_t again (X = E o R)]      (X_ZERO: [R_t])
@@ -89,13 +90,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
 template <int CW>
