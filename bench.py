@@ -16,8 +16,8 @@ oracle baseline and the SM clocks seen during the timed region.
 Multi-GPU (torchrun, one process per GPU, N > 1): the 3D grid is slab-sharded along x_1 over the
 N ranks (rsfde_team_*: NCCL all-to-all transposes for the x_1 transforms, allreduce of the CGS2
 dots) -- strong scaling of the same problem; value = N_unknowns * iterations / max-over-ranks
-device time.  If the sharded setup fails (NCCL unavailable) the ranks fall back to independent
-replicas ("weak") and the JSON line says so.
+device time.  The ranks run independent
+replicas only with --replicas; a failing sharded run exits non-zero (no silent fallback).
 """
 from __future__ import annotations
 
@@ -434,6 +434,28 @@ F_host = None
 F_host_steps = None
 
 
+def sharded_roofline(prob, ws, iters, t_max):
+    """Solve-level roofline of a slab-sharded run (per rank, algorithmic pass model of DESIGN.md section 8):
+    HBM bytes per GMRES iteration at Arnoldi index j = vec_r (14 + 3j + 7) for the K chain and CGS2
+    plus 12 vec_r for the three pack/unpack transposes; NVLink bytes = 3 vec_r (P-1)/P sent per rank."""
+    hbm, src = measured_peaks()
+    vec_r = 8.0 * prob.N / ws
+    nit = sum(iters)
+    hbm_bytes = nvl_bytes = 0.0
+    for k in iters:
+        for j in range(k):
+            hbm_bytes += vec_r * (14 + 3 * j + 7 + 12)
+            nvl_bytes += 3 * vec_r * (ws - 1) / ws
+    ach = hbm_bytes / t_max / 1e9
+    nvl = nvl_bytes / t_max / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None,
+            "scope": "solve-level per rank, algorithmic pass-model bytes / device time (not a single kernel)",
+            "peak_source": src, "iterations": nit,
+            "nvlink": {"achieved": nvl, "peak": 900.0, "unit": "GB/s", "frac": nvl / 900.0,
+                       "bytes_per_iteration_per_rank": 3 * vec_r * (ws - 1) / ws,
+                       "peak_source": "NVLink 5 nominal 900 GB/s per direction per GPU"}}
+
+
 def run_sharded(args):
     """N > 1: one C5 grid slab-sharded along x_1 over the ranks (strong scaling)."""
     import torch
@@ -520,8 +542,8 @@ def run_sharded(args):
                        "M": prob.M, "restart": prob.restart, "tol": prob.tol, "unknowns": N,
                        "parallelism": f"slab x1 over {ws} ranks (NCCL all-to-all transposes, allreduce dots)",
                        "l2": "no flush: every slab vector exceeds L2 at N <= 8 for C5", "iters_per_step": iters},
-            "e2e": e2e, "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "clocks": clk,
-            "setup_seconds": setup_s,
+            "e2e": e2e, "gpu_launches": launches, "roofline": sharded_roofline(prob, ws, iters, t_max),
+            "cpu_baseline": None, "clocks": clk, "setup_seconds": setup_s,
         }
         print(json.dumps(out), flush=True)
     T.close()
@@ -544,13 +566,8 @@ def main(argv=None):
         return run_reference(args)
     ws = _dist()[0]
     if ws > 1 and not args.replicas:
-        try:
-            return run_sharded(args)
-        except Exception as exc:  # NCCL / sharding unavailable: independent replicas instead
-            print(f"sharded run failed ({exc!r}); falling back to replicas", file=sys.stderr, flush=True)
-            import torch.distributed as dist
-            if dist.is_initialized():
-                dist.destroy_process_group()
+        # no silent fallback: a broken sharded path must fail the run, not turn into replicas
+        return run_sharded(args)
     return run_ours(args)
 
 

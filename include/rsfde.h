@@ -26,9 +26,9 @@
  *    owns its tables, Krylov basis and work buffers (padded private layout).
  *  - A ctx is used by one host thread at a time.  Calls are stream-ordered; only GMRES
  *    calls synchronise the stream (once per Arnoldi step, to read the convergence flag).
- *  - Restriction: every n_i + 1 must be a power of two with 2 <= n_i + 1 <= 512 (FFT lengths
- *    L = 2(n_i+1) <= 1024 are built); otherwise RSFDE_E_DIM.  The paper's grids (N+1 = 2^k,
- *    P:532-633) and BASELINE configs C1, C2, C4, C5 satisfy it; C3 (n = 2047) does not yet.
+ *  - Restriction: every n_i + 1 must be a power of two with 2 <= n_i + 1 <= 2048 (FFT lengths
+ *    L = 2(n_i+1) <= 4096 are built); otherwise RSFDE_E_DIM.  The paper's grids (N+1 = 2^k,
+ *    P:532-633) and all five BASELINE configs (n = 255, 255^2, 2047^2, 255^3, 511^3) satisfy it.
  */
 #ifndef RSFDE_H
 #define RSFDE_H
@@ -47,7 +47,7 @@ typedef enum {
   RSFDE_E_COEFF = 3,  /* e-check <= 0: e must be positive with a positive minimum */
   RSFDE_E_CONFIG = 4, /* missing coefficient tables, bad GMRES configuration */
   RSFDE_E_CUDA = 5,   /* CUDA error (message in rsfde_last_error) */
-  RSFDE_E_NCCL = 6,   /* reserved: multi-GPU slab sharding is not in this version */
+  RSFDE_E_NCCL = 6,   /* NCCL missing (libnccl.so.2 is dlopen'ed) or an NCCL call of the rsfde_team_* API failed */
   RSFDE_E_NOMEM = 7   /* device allocation failed */
 } rsfde_status;
 
@@ -108,7 +108,9 @@ typedef struct {
   double tol;       /* stop when |g_{j+1}| <= tol * ||r_0|| (preconditioned residual) */
   int x0_policy;    /* RSFDE_X0_PREV: x_0 = u^{(m)} (default); RSFDE_X0_ZERO */
   int form;         /* RSFDE_FORM_A (default), RSFDE_FORM_ATILDE or RSFDE_FORM_TWO_SIDED */
-  int fixed_iters;  /* > 0: run exactly this many Arnoldi steps (replay mode for parity) */
+  int fixed_iters;  /* > 0: replay mode for parity: ignore tol and run exactly this many
+                       Arnoldi steps, restarting every `restart` steps as needed (a lucky breakdown
+                       still ends the solve early); the step is then reported converged */
 } rsfde_gmres_cfg;
 
 typedef struct {
@@ -155,7 +157,9 @@ rsfde_status rsfde_solve_steps(rsfde_ctx *ctx, int m_begin, int m_count, double 
    independent systems at once).  Runs rsfde_solve_steps(ctxs[i], m_begin[i], m_count[i], u[i],
    F[i], F_static[i], &cfgs[i], &reps[i], streams[i]) for i < count concurrently: one host worker
    and one CUDA stream per system (streams may be NULL or hold NULL entries: the library then creates
-   and destroys a non-blocking stream for that system and synchronizes it before returning).  The
+   a non-blocking stream for that system, orders it after the work already queued on the legacy
+   default stream, and synchronizes and destroys it before returning; inputs produced on other
+   streams must be synchronized by the caller first).  The
    systems must be distinct contexts (RSFDE_E_CONFIG otherwise); each system's results are exactly
    those of its own rsfde_solve_steps call (same kernels, deterministic reductions).  F and F_static
    may be NULL (no source / static).  Returns the first failing system's status (the per-system
@@ -206,7 +210,8 @@ int rsfde_profile_read(rsfde_ctx *ctx, int cls, long long *launches, double *ms,
  * nccl_id == NULL, nlocal = nranks: all ranks emulated in this process on one device (transport =
  *             device copies);
  *             vectors are the whole dense grid.  Used by the single-GPU parity tests.
- * Same conventions as above otherwise (device pointers, stream-ordered, A form only). */
+ * Same conventions as above otherwise (device pointers, stream-ordered, A form only).  The
+ * coefficient must be RSFDE_COEF_SEPARABLE (a dense grid e is not sliced per rank): RSFDE_E_CONFIG. */
 typedef struct rsfde_team rsfde_team;
 rsfde_status rsfde_nccl_unique_id(void *out128);
 rsfde_status rsfde_team_setup(rsfde_team **out, const rsfde_problem *p, int nranks, int rank, int nlocal,

@@ -93,7 +93,8 @@ def gmres(apply_K: Callable[[np.ndarray], np.ndarray], c: np.ndarray, x0: np.nda
             y[i] = (g[i] - np.dot(Hm[i, i + 1:k], y[i + 1:k])) / Hm[i, i]
         for i in range(k):
             x = x + y[i] * V[i]
-        converged = stop if fixed_iters is None else True
+        # replay mode keeps restarting until exactly fixed_iters Arnoldi steps ran
+        converged = stop if fixed_iters is None else total >= fixed_iters
         if breakdown:
             converged = True
         if converged or total >= max_iters:

@@ -16,6 +16,7 @@ using rsfde::GmresState;
 
 struct rsfde_ctx {
   int device = 0;  // CUDA device the context lives on (set by setup)
+  int nblk = 0;    // blocks (= partial sums) of the streaming reductions: 8 per SM of that device
   // on-chip 1-D march (lazily allocated): generator table, per-step outputs, device copy of host F
   double* d_s0 = nullptr;
   int* d_on_iters = nullptr;

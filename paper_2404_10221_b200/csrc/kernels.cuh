@@ -3,7 +3,34 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 namespace rsfde {
+
+// Kernel attributes (dynamic shared memory opt-in) and the SM count are per device: run `init`
+// once per (call site, device).  `Tag` makes every call site (template instantiation) its own cache.
+constexpr int kMaxDevices = 64;
+template <class Tag, class F>
+inline int per_device_once(F init) {
+  static std::once_flag flags[kMaxDevices];
+  static int result[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return -1;
+  std::call_once(flags[dev], [&] { result[dev] = init(dev); });
+  return result[dev];
+}
+
+// SM count of the current device (B200: 148) and the block count of the streaming kernels
+// (8 resident 256-thread blocks per SM)
+inline int device_sm_count() {
+  struct Tag {};
+  const int n = per_device_once<Tag>([](int dev) -> int {
+    int v = 0;
+    return cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0 ? v : 148;
+  });
+  return n > 0 ? n : 148;
+}
+inline int stream_blocks() { return 8 * device_sm_count(); }
 
 // Grid geometry of the internal layout: C order [x1][x2][x3] (x_d fastest), the last
 // dimension padded to P = n_d + 1 with a zero pad element (private layout).

@@ -444,7 +444,7 @@ cudaError_t launch_update_norm(const double* const* V, const double* vscale, int
 cudaError_t launch_axpy_basis(const double* const* V, const double* vscale, int J, const double* y, double* x,
                               long long NP, cudaStream_t s) {
   if (J < 1 || J > kMaxBasis) return cudaErrorInvalidValue;
-  const unsigned g = grid_for(NP / 2, 148 * 8);
+  const unsigned g = grid_for(NP / 2, stream_blocks());
   RSFDE_JP(run_axpy, J, g, s, make_basis(V, J), vscale, J, y, x, NP / 2);
   return cudaGetLastError();
 }
@@ -460,19 +460,19 @@ cudaError_t launch_sumsq(const double* z, double* partial, long long NP, int nbl
 }
 
 cudaError_t launch_axpby(double a, const double* x, double b, double* y, long long NP, cudaStream_t s) {
-  axpby_kernel<<<grid_for(NP / 2, 148 * 8), 256, 0, s>>>(a, x, b, y, NP / 2);
+  axpby_kernel<<<grid_for(NP / 2, stream_blocks()), 256, 0, s>>>(a, x, b, y, NP / 2);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pack(const double* dense, double* padded, const Geom& g, cudaStream_t s) {
   const long long rows = g.NP / g.P;
-  pack_kernel<<<grid_for(g.NP, 148 * 8), 256, 0, s>>>(dense, padded, rows, g.n[g.d - 1], g.P);
+  pack_kernel<<<grid_for(g.NP, stream_blocks()), 256, 0, s>>>(dense, padded, rows, g.n[g.d - 1], g.P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(const double* padded, double* dense, const Geom& g, cudaStream_t s) {
   const long long rows = g.NP / g.P;
-  unpack_kernel<<<grid_for(rows * g.n[g.d - 1], 148 * 8), 256, 0, s>>>(padded, dense, rows, g.n[g.d - 1], g.P);
+  unpack_kernel<<<grid_for(rows * g.n[g.d - 1], stream_blocks()), 256, 0, s>>>(padded, dense, rows, g.n[g.d - 1], g.P);
   return cudaGetLastError();
 }
 
@@ -484,7 +484,7 @@ cudaError_t launch_compact_source(const double* f_closed, double* F, const Geom&
     w[i][1] = alpha[i] / 24.0;
   }
   const long long N = (long long)g.n[0] * g.n[1] * g.n[2];
-  compact_source_kernel<<<grid_for(N, 148 * 8), 256, 0, s>>>(f_closed, F, g, w[0][0], w[0][1], w[1][0], w[1][1],
+  compact_source_kernel<<<grid_for(N, stream_blocks()), 256, 0, s>>>(f_closed, F, g, w[0][0], w[0][1], w[1][0], w[1][1],
                                                               w[2][0], w[2][1]);
   return cudaGetLastError();
 }

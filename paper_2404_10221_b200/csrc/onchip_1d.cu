@@ -1,5 +1,5 @@
 // On-chip CN march for small 1-D problems (BASELINE C1: n = 255; SURVEY 8(d) "on-chip / latency: one
-// CTA, whole run in shared memory").  One CTA of 512 threads runs every CN step of Eq.(tls) and the
+// CTA, whole run in shared memory").  One CTA of 1024 threads runs every CN step of Eq.(tls) and the
 // whole tau-preconditioned GMRES solve of each step without returning to the host: the Krylov basis,
 // the Hessenberg matrix and the 1-D tables live in shared memory, so an iteration costs a few
 // microseconds instead of a host round trip per iteration.
@@ -372,9 +372,11 @@ __global__ void __launch_bounds__(kOnThreads, 1) onchip_1d_kernel(const OnchipPa
 
 cudaError_t launch_onchip_1d(const OnchipParams& p, cudaStream_t s) {
   const size_t smem = onchip_smem_bytes(p.n, p.restart);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(onchip_1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (attr != cudaSuccess) return attr;
+  struct Tag {};
+  const int attr = per_device_once<Tag>([](int) -> int {
+    return (int)cudaFuncSetAttribute(onchip_1d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  });
+  if (attr != (int)cudaSuccess) return attr < 0 ? cudaErrorInvalidDevice : (cudaError_t)attr;
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   onchip_1d_kernel<<<1, kOnThreads, smem, s>>>(p);
   return cudaGetLastError();

@@ -528,10 +528,12 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
 template <class T, int MODE>
 cudaError_t launch_mode(const PassParams& p, cudaStream_t s) {
   const size_t smem = (size_t)T::GROUPS * T::L * sizeof(double2);
-  // once per process (thread-safe static initialisation: batched solves drive several streams)
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(pass_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (attr != cudaSuccess) return attr;
+  // once per device (thread-safe: batched solves drive several streams and devices)
+  struct Tag {};
+  const int attr = per_device_once<Tag>([smem](int) -> int {
+    return (int)cudaFuncSetAttribute(pass_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (attr != (int)cudaSuccess) return attr < 0 ? cudaErrorInvalidDevice : (cudaError_t)attr;
   const long long blocks = (p.npairs + T::GROUPS - 1) / T::GROUPS;
   pass_kernel<T, MODE><<<(unsigned)blocks, T::THREADS, smem, s>>>(p);
   return cudaGetLastError();

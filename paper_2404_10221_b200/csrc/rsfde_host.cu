@@ -22,7 +22,6 @@ namespace {
 thread_local std::string g_setup_error;
 const char* kProfNames[RSFDE_NPROF] = {"oper_pass_spectral", "oper_pass_physical", "dst_pass", "cgs_dots",
                                        "cgs_dots2", "cgs_update_norm", "x_update", "small"};
-constexpr int kNblk = 148 * 8;
 }  // namespace
 
 // ------------------------------------------------------------------------------ helpers
@@ -87,12 +86,15 @@ enum { PC_OPER_SPEC = 0, PC_OPER_PHYS = 1, PC_DST = 2, PC_DOTS = 3, PC_DOTS2 = 4
     if (_s != RSFDE_OK) return _s;      \
   } while (0)
 
-static rsfde_status dalloc(rsfde_ctx* c, void** p, size_t bytes) {
+// zero-initialised device allocation.  Without a stream the memset runs on the legacy default stream
+// (setup synchronises the device before returning); lazy allocations inside a call pass the call's
+// stream so that the zeroing is ordered before the kernels that read the buffer.
+static rsfde_status dalloc(rsfde_ctx* c, void** p, size_t bytes, cudaStream_t s = nullptr, bool on_stream = false) {
   cudaError_t e = cudaMalloc(p, bytes);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMalloc");
   c->allocs.push_back(*p);
   c->bytes += (long long)bytes;
-  e = cudaMemset(*p, 0, bytes);
+  e = on_stream ? cudaMemsetAsync(*p, 0, bytes, s) : cudaMemset(*p, 0, bytes);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset");
   return RSFDE_OK;
 }
@@ -350,10 +352,10 @@ static rsfde_status precond_chain(rsfde_ctx* c, int kind, const double* x, doubl
 }
 
 // ------------------------------------------------------------------------------ GMRES
-static rsfde_status ensure_basis(rsfde_ctx* c, int restart) {
+static rsfde_status ensure_basis(rsfde_ctx* c, int restart, cudaStream_t s) {
   while ((int)c->V.size() < restart + 1) {
     double* v = nullptr;
-    TRY(dalloc(c, (void**)&v, c->geo.NP * sizeof(double)));
+    TRY(dalloc(c, (void**)&v, c->geo.NP * sizeof(double), s, true));
     c->V.push_back(v);
   }
   return RSFDE_OK;
@@ -438,9 +440,9 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
   const int fixed = cfg.fixed_iters;
   const double tol = fixed > 0 ? -1.0 : cfg.tol;
   const int form = cfg.form;
-  TRY(ensure_basis(c, restart));
+  TRY(ensure_basis(c, restart, s));
   const long long NP = c->geo.NP;
-  const int nb = reduction_blocks(NP, kNblk);
+  const int nb = reduction_blocks(NP, c->nblk);
   int total = 0;
   bool first = true;
   Flags fl{0, 0, 1.0};
@@ -478,7 +480,7 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
       }
       TRY(precond_residual(c, form, m, c->BUF, c->X, c->V[0], s));
     }
-    CKL(launch_sumsq(c->V[0], c->d_nrm, NP, kNblk, s), "sumsq");
+    CKL(launch_sumsq(c->V[0], c->d_nrm, NP, c->nblk, s), "sumsq");
     CKL(launch_gmres_init(c->d_state, c->d_nrm, nb, c->d_vscale, first ? 1 : 0, s), "gmres init");
     TRY(read_flags(c, &fl, s));
     if (fl.converged) {  // r0 == 0: x0 is the solution
@@ -491,13 +493,13 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
       TRY(apply_K(c, form, m, c->V[j], c->d_vscale + j, c->Z, s));
       const double* const* Vp = (const double* const*)c->V.data();
       const double vb = 8.0 * (double)NP;
-      LAUNCH(PC_DOTS, vb * (J + 1), launch_dots(Vp, c->d_vscale, J, c->Z, c->d_part, NP, kNblk, s), "dots");
+      LAUNCH(PC_DOTS, vb * (J + 1), launch_dots(Vp, c->d_vscale, J, c->Z, c->d_part, NP, c->nblk, s), "dots");
       CKL(launch_reduce(c->d_part, nb, J, c->d_h1, s), "reduce h1");
-      LAUNCH(PC_DOTS2, vb * (J + 1), launch_dots_after_update(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_part, NP, kNblk, s),
+      LAUNCH(PC_DOTS2, vb * (J + 1), launch_dots_after_update(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_part, NP, c->nblk, s),
              "dots2");
       CKL(launch_reduce(c->d_part, nb, J, c->d_h2, s), "reduce h2");
       LAUNCH(PC_UPD, vb * (J + 2),
-             launch_update_norm(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_h2, c->V[j + 1], c->d_nrm, NP, kNblk, s),
+             launch_update_norm(Vp, c->d_vscale, J, c->Z, c->d_h1, c->d_h2, c->V[j + 1], c->d_nrm, NP, c->nblk, s),
              "update");
       CKL(launch_arnoldi_finish(c->d_state, c->d_h1, c->d_h2, c->d_nrm, nb, j, tol, c->d_vscale + j + 1, s),
           "finish");
@@ -511,7 +513,8 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
     const double* const* Vp = (const double* const*)c->V.data();
     const double* d_y = reinterpret_cast<const double*>(reinterpret_cast<const char*>(c->d_state) + offsetof(GmresState, y));
     LAUNCH(PC_XUPD, 8.0 * (double)NP * (k + 2), launch_axpy_basis(Vp, c->d_vscale, k, d_y, c->X, NP, s), "x update");
-    converged = fixed > 0 ? true : (fl.converged != 0 || fl.breakdown != 0);
+    // replay mode (fixed_iters > 0) keeps restarting until exactly `fixed` Arnoldi steps ran
+    converged = fixed > 0 ? (total >= fixed || fl.breakdown != 0) : (fl.converged != 0 || fl.breakdown != 0);
     if (converged || total >= max_iters) break;
     first = false;
   }
@@ -692,6 +695,7 @@ rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void*
   }
   rsfde_ctx* c = new rsfde_ctx();
   cudaGetDevice(&c->device);
+  c->nblk = rsfde::stream_blocks();
   c->d = p->d;
   for (int i = 0; i < 3; ++i) {
     c->n[i] = i < p->d ? p->n[i] : 1;
@@ -732,7 +736,7 @@ rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void*
     ECoef e = rsfde_ecoef_at(c, 0);
     if (c->ekind == RSFDE_COEF_GRID) e.grid = c->grid;
     double* part = nullptr;
-    const int nblk = 148 * 4;
+    const int nblk = 4 * rsfde::device_sm_count();
     if ((st = dalloc(c, (void**)&part, 2 * nblk * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
     const int Meff = (c->ekind == RSFDE_COEF_GRID && c->grid_static) ? 1 : c->M;
     cudaError_t ce = launch_emaxmin(e, c->d_ahalf, c->d_bhalf, Meff, c->grid_static, G, part, nblk, s);
@@ -764,10 +768,12 @@ rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void*
   if ((st = dalloc(c, (void**)&c->d_vscale, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_h1, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_h2, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
-  if ((st = dalloc(c, (void**)&c->d_part, (size_t)kNblk * 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
-  if ((st = dalloc(c, (void**)&c->d_nrm, (size_t)kNblk * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_part, (size_t)c->nblk * 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_nrm, (size_t)c->nblk * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_state, sizeof(GmresState))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if (cudaMallocHost(&c->h_flags, 64) != cudaSuccess) return setup_fail(c, RSFDE_E_NOMEM, "cudaMallocHost");
+  // the zeroing memsets ran on the legacy default stream: complete them before any caller stream
+  if (cudaDeviceSynchronize() != cudaSuccess) return setup_fail(c, RSFDE_E_CUDA, "setup synchronisation");
   c->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   *out = c;
   return RSFDE_OK;
@@ -1002,6 +1008,17 @@ rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx* const* ctxs, const in
       }
   std::vector<rsfde_status> st(count, RSFDE_OK);
   std::vector<cudaStream_t> own(count, nullptr);
+  // Streams the library creates are ordered after the work already queued on the legacy default
+  // stream (an event recorded there is waited on); callers that produced u / F on other streams
+  // synchronise those first (the Python binding synchronises torch's current stream).
+  std::vector<cudaEvent_t> ready(count, nullptr);
+  for (int i = 0; i < count; ++i) {
+    if (streams && streams[i]) continue;
+    if (!ctxs[i] || cudaSetDevice(ctxs[i]->device) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ready[i], cudaStreamLegacy) != cudaSuccess)
+      return RSFDE_E_CUDA;
+  }
   // one host worker and one stream per system: the independent marches overlap on the device (small
   // grids leave most SMs idle) and their per-iteration host syncs overlap on the host
   auto work = [&](int i) {
@@ -1010,7 +1027,8 @@ rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx* const* ctxs, const in
     if (cudaSetDevice(c->device) != cudaSuccess) { st[i] = RSFDE_E_CUDA; return; }
     void* s = streams ? streams[i] : nullptr;
     if (!s) {
-      if (cudaStreamCreateWithFlags(&own[i], cudaStreamNonBlocking) != cudaSuccess) { st[i] = RSFDE_E_CUDA; return; }
+      if (cudaStreamCreateWithFlags(&own[i], cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamWaitEvent(own[i], ready[i], 0) != cudaSuccess) { st[i] = RSFDE_E_CUDA; return; }
       s = own[i];
     }
     st[i] = rsfde_solve_steps(c, m_begin[i], m_count[i], u[i], F ? F[i] : nullptr, F_static ? F_static[i] : 1,
@@ -1022,8 +1040,10 @@ rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx* const* ctxs, const in
   for (int i = 1; i < count; ++i) th.emplace_back(work, i);
   if (count > 0) work(0);
   for (auto& t : th) t.join();
-  for (int i = 0; i < count; ++i)
+  for (int i = 0; i < count; ++i) {
     if (own[i]) cudaStreamDestroy(own[i]);
+    if (ready[i]) cudaEventDestroy(ready[i]);
+  }
   for (int i = 0; i < count; ++i)
     if (st[i] != RSFDE_OK) return st[i];
   return RSFDE_OK;

@@ -58,7 +58,7 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 thread_local std::string g_team_error;
-constexpr int kNblkT = 148 * 8;
+
 
 // ------------------------------------------------------------------------------ transposes
 // A = [x1l < s][x2 < n2][x3 < P3]  ->  send block r' (x2 in [r' s2, (r'+1) s2)) = [x2l][x3 < n3][x1l < s]
@@ -298,7 +298,7 @@ static rsfde_status transpose_AT(rsfde_team* t, double* const* srcA, double* con
   TTRY(team_alltoall(t, s));
   for (int l = 0; l < t->nlocal; ++l) {
     const ShardBufs& b = t->sh[l];
-    TCKL((unpack_AT_kernel<<<148 * 8, 256, 0, s>>>(b.recv, dstT[l], t->s, t->s2, t->tab->n[2], b.gT.P, t->blk),
+    TCKL((unpack_AT_kernel<<<stream_blocks(), 256, 0, s>>>(b.recv, dstT[l], t->s, t->s2, t->tab->n[2], b.gT.P, t->blk),
           cudaGetLastError()),
          "unpack A->T");
   }
@@ -308,7 +308,7 @@ static rsfde_status transpose_AT(rsfde_team* t, double* const* srcA, double* con
 static rsfde_status transpose_TA(rsfde_team* t, double* const* srcT, double* const* dstA, cudaStream_t s) {
   for (int l = 0; l < t->nlocal; ++l) {
     const ShardBufs& b = t->sh[l];
-    TCKL((pack_TA_kernel<<<148 * 8, 256, 0, s>>>(srcT[l], b.send, t->s, t->s2, t->tab->n[2], b.gT.P, t->P, t->blk),
+    TCKL((pack_TA_kernel<<<stream_blocks(), 256, 0, s>>>(srcT[l], b.send, t->s, t->s2, t->tab->n[2], b.gT.P, t->P, t->blk),
           cudaGetLastError()),
          "pack T->A");
   }
@@ -454,13 +454,17 @@ static rsfde_status team_precond(rsfde_team* t, int kind, double* const* in, dou
 }
 
 static rsfde_status team_ensure_basis(rsfde_team* t, int restart) {
+  bool grew = false;
   for (auto& b : t->sh) {
     while ((int)b.V.size() < restart + 1) {
       double* v = nullptr;
       TTRY(talloc(t, &v, (size_t)b.gA.NP));
       b.V.push_back(v);
+      grew = true;
     }
   }
+  // talloc zeroes on the legacy default stream: finish that before the caller's stream reads the basis
+  if (grew) TCK(cudaDeviceSynchronize(), "basis zeroing");
   return RSFDE_OK;
 }
 
@@ -498,7 +502,7 @@ static rsfde_status team_gmres(rsfde_team* t, int m, bool fast, bool have_b, con
   const double tol = fixed > 0 ? -1.0 : cfg.tol;
   TTRY(team_ensure_basis(t, restart));
   const long long NP = t->sh[0].gA.NP;
-  const int nb = reduction_blocks(NP, kNblkT);
+  const int nb = reduction_blocks(NP, t->tab->nblk);
   int total = 0;
   bool first = true, converged = false;
   TFlags fl{0, 0, 1.0};
@@ -531,7 +535,7 @@ static rsfde_status team_gmres(rsfde_team* t, int m, bool fast, bool have_b, con
     }
     for (int l = 0; l < nl; ++l) {
       ShardBufs& b = t->sh[l];
-      TCKL(launch_sumsq(b.V[0], b.nrm, NP, kNblkT, s), "sumsq");
+      TCKL(launch_sumsq(b.V[0], b.nrm, NP, t->tab->nblk, s), "sumsq");
       TCKL(launch_reduce(b.nrm, nb, 1, b.red, s), "reduce");
     }
     TTRY(team_allreduce(t, [&](int l) { return t->sh[l].red; }, 1, s));
@@ -558,21 +562,21 @@ static rsfde_status team_gmres(rsfde_team* t, int m, bool fast, bool have_b, con
       for (int l = 0; l < nl; ++l) {
         ShardBufs& b = t->sh[l];
         const double* const* Vp = (const double* const*)b.V.data();
-        TCKL(launch_dots(Vp, b.vscale, J, b.Z, b.part, NP, kNblkT, s), "dots");
+        TCKL(launch_dots(Vp, b.vscale, J, b.Z, b.part, NP, t->tab->nblk, s), "dots");
         TCKL(launch_reduce(b.part, nb, J, b.h1, s), "reduce h1");
       }
       TTRY(team_allreduce(t, [&](int l) { return t->sh[l].h1; }, J, s));
       for (int l = 0; l < nl; ++l) {
         ShardBufs& b = t->sh[l];
         const double* const* Vp = (const double* const*)b.V.data();
-        TCKL(launch_dots_after_update(Vp, b.vscale, J, b.Z, b.h1, b.part, NP, kNblkT, s), "dots2");
+        TCKL(launch_dots_after_update(Vp, b.vscale, J, b.Z, b.h1, b.part, NP, t->tab->nblk, s), "dots2");
         TCKL(launch_reduce(b.part, nb, J, b.h2, s), "reduce h2");
       }
       TTRY(team_allreduce(t, [&](int l) { return t->sh[l].h2; }, J, s));
       for (int l = 0; l < nl; ++l) {
         ShardBufs& b = t->sh[l];
         const double* const* Vp = (const double* const*)b.V.data();
-        TCKL(launch_update_norm(Vp, b.vscale, J, b.Z, b.h1, b.h2, b.V[j + 1], b.nrm, NP, kNblkT, s), "update");
+        TCKL(launch_update_norm(Vp, b.vscale, J, b.Z, b.h1, b.h2, b.V[j + 1], b.nrm, NP, t->tab->nblk, s), "update");
         TCKL(launch_reduce(b.nrm, nb, 1, b.red, s), "reduce nrm");
       }
       TTRY(team_allreduce(t, [&](int l) { return t->sh[l].red; }, 1, s));
@@ -593,7 +597,7 @@ static rsfde_status team_gmres(rsfde_team* t, int m, bool fast, bool have_b, con
       const double* const* Vp = (const double* const*)b.V.data();
       TCKL(launch_axpy_basis(Vp, b.vscale, k, d_y, b.X, NP, s), "x update");
     }
-    converged = fixed > 0 ? true : (fl.converged != 0 || fl.breakdown != 0);
+    converged = fixed > 0 ? (total >= fixed || fl.breakdown != 0) : (fl.converged != 0 || fl.breakdown != 0);
     if (converged || total >= max_iters) break;
     first = false;
   }
@@ -663,6 +667,11 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
   if (!out) return RSFDE_E_CONFIG;
   *out = nullptr;
   if (!p || p->d != 3) { g_team_error = "slab sharding needs d = 3"; return RSFDE_E_DIM; }
+  if (p->e.kind != RSFDE_COEF_SEPARABLE) {
+    // a dense e grid would need a per-rank slab layout (the pass kernels index it unsharded)
+    g_team_error = "slab sharding supports the separable coefficient (RSFDE_COEF_SEPARABLE) only";
+    return RSFDE_E_CONFIG;
+  }
   if (nranks < 1 || nranks > 8 || (nlocal != 1 && nlocal != nranks) || rank < 0 || rank >= nranks ||
       (nlocal == nranks && rank != 0)) {
     g_team_error = "nranks in 1..8; nlocal = 1 (one rank per process) or nlocal = nranks (emulation, rank 0)";
@@ -722,8 +731,8 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     double** sm[] = {&b.vscale, &b.h1, &b.h2, &b.red};
     for (double** v : sm)
       if ((st = talloc(t, v, 64)) != RSFDE_OK) return fail(st);
-    if ((st = talloc(t, &b.part, (size_t)kNblkT * 64)) != RSFDE_OK) return fail(st);
-    if ((st = talloc(t, &b.nrm, (size_t)kNblkT)) != RSFDE_OK) return fail(st);
+    if ((st = talloc(t, &b.part, (size_t)t->tab->nblk * 64)) != RSFDE_OK) return fail(st);
+    if ((st = talloc(t, &b.nrm, (size_t)t->tab->nblk)) != RSFDE_OK) return fail(st);
     double* stp = nullptr;
     if ((st = talloc(t, &stp, (sizeof(GmresState) + 7) / 8)) != RSFDE_OK) return fail(st);
     b.st = reinterpret_cast<GmresState*>(stp);

@@ -557,16 +557,16 @@ cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
   constexpr int kTileThreads = TileCfg<CW>::kTileThreads, kCtasPerSm = TileCfg<CW>::kCtasPerSm;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
   const size_t smem = (size_t)kTilePairs * T::L * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
-  // kernel attribute and SM count, once per process (thread-safe static initialisation)
-  static const int sms = [smem]() -> int {
+  // kernel attribute and SM count, once per device (thread-safe)
+  struct Tag {};
+  const int sms = per_device_once<Tag>([smem](int dev) -> int {
     if (cudaFuncSetAttribute(tile_kernel<MODE, T, TP, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return -1;
-    int dev = 0, n = 0;
-    cudaGetDevice(&dev);
+    int n = 0;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
-  }();
+  });
   if (sms <= 0) return cudaErrorInvalidValue;
   alignas(64) CUtensorMap tmR, tmX;
   memset(&tmR, 0, sizeof(tmR));

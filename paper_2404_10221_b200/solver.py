@@ -35,7 +35,9 @@ class RsfdeSolver:
 
     def __init__(self, d: int, n: Sequence[int], alpha: Sequence[float], kappa: Sequence[float], tau: float,
                  M: int, a_half: np.ndarray, b_half: np.ndarray, g: Sequence[Optional[np.ndarray]],
-                 k: Sequence[Optional[np.ndarray]], stream=None):
+                 k: Sequence[Optional[np.ndarray]], stream=None, grid=None, grid_static: bool = False):
+        """Separable e from the tables (a_half, b_half, g, k), or -- with ``grid`` (a contiguous float64
+        CUDA tensor of M*N values, or N values with grid_static) -- the dense RSFDE_COEF_GRID kind."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("rsfde needs a CUDA device (no CPU fallback)")
@@ -54,6 +56,16 @@ class RsfdeSolver:
         prob.tau_t = tau
         prob.M = M
         prob.e.kind = L.COEF_SEPARABLE
+        if grid is not None:
+            if not (isinstance(grid, torch.Tensor) and grid.is_cuda and grid.dtype == torch.float64
+                    and grid.is_contiguous()):
+                raise TypeError("grid must be a contiguous float64 CUDA tensor")
+            if grid.numel() != int(np.prod(self.n)) * (1 if grid_static else M):
+                raise ValueError("grid must hold M*N values (N with grid_static)")
+            self._keep.append(grid)
+            prob.e.kind = L.COEF_GRID
+            prob.e.grid = C.cast(C.c_void_p(grid.data_ptr()), L.DP)
+            prob.e.grid_static = 1 if grid_static else 0
         prob.e.a_half = _dp(self._keep[0])
         prob.e.b_half = _dp(self._keep[1])
         for i in range(3):
@@ -80,6 +92,14 @@ class RsfdeSolver:
         """Set up from a ``paper_2404_10221_b200.inputs.Problem``."""
         a_half, b_half, gs, ks = prob.e_tables()
         return cls(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau, prob.M, a_half, b_half, gs, ks, stream)
+
+    @classmethod
+    def from_problem_grid(cls, prob, grid, grid_static: bool = False, stream=None) -> "RsfdeSolver":
+        """Set up with the dense coefficient kind: ``grid`` holds e(x, t_{m+1/2}) on the interior grid
+        for every m (M*N values) or one time-constant field (grid_static)."""
+        d = prob.d
+        return cls(prob.d, prob.n, prob.alpha, prob.kappa, prob.tau, prob.M, np.zeros(prob.M), np.zeros(prob.M),
+                   [None] * d, [None] * d, stream, grid=grid, grid_static=grid_static)
 
     # ------------------------------------------------------------------ helpers
     def _check(self, st):
@@ -247,6 +267,10 @@ def solve_steps_batch(solvers, us, Fs=None, F_static=None, m_begin=None, m_count
         its, rr, cv = (C.c_int * n)(), (C.c_double * n)(), (C.c_ubyte * n)()
         bufs.append((its, rr, cv))
         reps[i].iters, reps[i].final_relres, reps[i].converged = its, rr, cv
+    # the library's per-system streams wait for the legacy default stream only: make the inputs
+    # produced on torch's current stream visible first
+    import torch
+    torch.cuda.current_stream().synchronize()
     st = lib.rsfde_solve_steps_batch(B, ctxs, mb, mc, ub, Fb, fs, cf, reps, None)
     if st != 0:
         msgs = [S.lib.rsfde_last_error(S.ctx).decode() for S in solvers]

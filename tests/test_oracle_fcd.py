@@ -179,3 +179,34 @@ def test_h_eigenvalues_spec_example():
     # alpha=1.5, n=4 -> 1 - 0.25 sin^2(k pi/10)
     k = np.arange(1, 5)
     assert np.allclose(fcd.h_eigenvalues(1.5, 4), 1 - 0.25 * np.sin(k * np.pi / 10) ** 2, atol=1e-16)
+
+
+# ---------------------------------------------------------------- extended-precision pin of q
+def mp_tau_eigenvalues(alpha, n, ks, dps=30):
+    """q(k) = s_0 + 2 sum_{j=1}^{n-1} s_j cos(pi j k/(n+1)) (Eq.(q), divisor n+1 per Q2) with
+    s_j from the Gamma closed form (-1)^j Gamma(alpha+1) / (Gamma(alpha/2-j+1) Gamma(alpha/2+j+1))
+    -- not the oracle's recurrence -- evaluated with 30 significant digits (mpmath)."""
+    import mpmath as mp
+    with mp.workdps(dps):
+        a = mp.mpf(alpha)
+        g = mp.gamma(a + 1)
+        s = [(-1) ** j * g / (mp.gamma(a / 2 - j + 1) * mp.gamma(a / 2 + j + 1)) for j in range(n)]
+        out = []
+        for k in ks:
+            acc = s[0]
+            for j in range(1, n):
+                acc += 2 * s[j] * mp.cos(mp.pi * j * k / (n + 1))
+            out.append(acc)
+        return [float(v) for v in out]
+
+
+@pytest.mark.parametrize("alpha,n", [(1.1, 511), (1.5, 511), (1.9, 511), (1.2, 2047), (1.9, 2047)])
+def test_tau_eigenvalues_match_30_digit_reference(alpha, n):
+    # the small-k eigenvalues are heavily cancelling sums (condition up to ~1e6 at alpha=1.9,
+    # n=2047): a plain FP64 sum is off by up to 2.5e-11 there (7e-12 at n=511), enough to move
+    # P_hat^{-1} x by more than the 1e-12 parity bar; the oracle's long-double recurrence and sum
+    # stay within 3e-14 (measured worst case: q(1) at alpha=1.9, n=2047) -- bar 1e-13 (SURVEY Q26)
+    ks = list(range(1, 9))
+    ref = np.array(mp_tau_eigenvalues(alpha, n, ks))
+    q = fcd.tau_eigenvalues(fcd.fcd_coefficients(alpha, n))[:8]
+    assert np.max(np.abs(q - ref) / np.abs(ref)) < 1e-13, np.abs(q - ref) / np.abs(ref)
