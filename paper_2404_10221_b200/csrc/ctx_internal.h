@@ -10,6 +10,7 @@
 #include "kernels.cuh"
 
 #define RSFDE_NPROF 8
+enum { ORTHO_DCGS2 = 0, ORTHO_CGS2 = 1 };
 
 using rsfde::Geom;
 using rsfde::GmresState;
@@ -17,6 +18,9 @@ using rsfde::GmresState;
 struct rsfde_ctx {
   int device = 0;  // CUDA device the context lives on (set by setup)
   int nblk = 0;    // blocks (= partial sums) of the streaming reductions: 8 per SM of that device
+  int ortho = 0;   // ORTHO_DCGS2 | ORTHO_CGS2
+  const int* skip = nullptr;             // device flags of the speculative Arnoldi launches (PassParams::skip)
+  cudaEvent_t flag_ev[2] = {nullptr, nullptr};  // flags copies of the last two Arnoldi steps
   // on-chip 1-D march (lazily allocated): generator table, per-step outputs, device copy of host F
   double* d_s0 = nullptr;
   int* d_on_iters = nullptr;

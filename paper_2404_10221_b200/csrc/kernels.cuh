@@ -120,7 +120,13 @@ struct PassParams {
   // global coordinate on a non-pass axis is >= cext are zero pads (never stored)
   int coff[3];
   int cext[3];
+  // speculative Arnoldi launches: when non-null and skip[0] | skip[1] (the GmresState converged /
+  // breakdown flags) is set, the kernel returns at once (see gmres_core in rsfde_host.cu)
+  const int* skip;
 };
+__device__ __forceinline__ bool skip_launch(const int* skip) {
+  return skip && ((*(volatile const int*)skip) | (*((volatile const int*)skip + 1)));
+}
 enum { PASS_FLAG_NO_PIPE = 1 };
 
 // host-side launchers (pass_kernels.cu)
@@ -173,6 +179,14 @@ struct GmresState {
   double g[52];
   double y[51];
   double hsum[52];      // h1 + h2 of the current column
+  // DCGS2 (delayed re-orthogonalisation): the unrotated Hessenberg matrix (column j tentative until
+  // the next iteration corrects it), g before the tentative rotation of each column, the update
+  // coefficients of the current iteration and the Pythagorean norm nu of the re-orthogonalised vector
+  double Hraw[52 * 51];
+  double gsave[52];
+  double cq[52], cu[52];
+  double nu;
+  int kcols;            // columns usable by the y solve (j+1, or j after a breakdown in the correction)
 };
 // number of blocks (= partial sums) every streaming reduction uses for a vector of length NP
 int reduction_blocks(long long NP, int nblk);
@@ -185,5 +199,21 @@ cudaError_t launch_gmres_init(GmresState* st, const double* partial_nrm, int nbl
                               int first_cycle, cudaStream_t s);
 // y = R^{-1} g for k columns
 cudaError_t launch_gmres_solve_y(GmresState* st, int k, cudaStream_t s);
+
+// ---- DCGS2 Arnoldi (one dots pass + one update pass per iteration, krylov_kernels.cu)
+// Iteration j: u = s_j V_j is the once-orthogonalised (lazily normalised) new vector, w = K u.
+// dots: partial[b*NT + t], NT = 2j+2: t < j: V_i.V_j, j <= t < 2j: V_i.w, 2j: V_j.V_j, 2j+1: V_j.w
+cudaError_t launch_dcgs_dots(const double* const* V, int j, const double* w, double* partial, long long NP,
+                             int nblk, const int* skip, cudaStream_t s);
+// reduce the dots, re-orthogonalise V_j (Pythagorean norm), correct and re-rotate Hessenberg column
+// j-1, form the tentative column j and the update coefficients (st->cq, st->cu)
+cudaError_t launch_dcgs_finish_a(GmresState* st, const double* partial, int nblk, int j, double* vscale,
+                                 const int* skip, cudaStream_t s);
+// V_j <- q_j = sum_i cq_i V_i (j > 0, in place), V_{j+1} <- w + sum_i cu_i V_i, ||V_{j+1}||^2 partials
+cudaError_t launch_dcgs_update(const double* const* V, int j, const GmresState* st, const double* w,
+                               double* partial_nrm, long long NP, int nblk, const int* skip, cudaStream_t s);
+// tentative subdiagonal h_{j+1,j}, rotation of column j, convergence flag, vscale[j+1]
+cudaError_t launch_dcgs_finish_b(GmresState* st, const double* partial_nrm, int nblk, int j, double tol,
+                                 double* vscale, const int* skip, cudaStream_t s);
 
 }  // namespace rsfde

@@ -259,17 +259,265 @@ __global__ void gmres_init_kernel(GmresState* st, const double* __restrict__ pnr
   st->relres = st->beta0 > 0.0 ? beta / st->beta0 : 0.0;
   st->converged = (beta == 0.0) ? 1 : 0;
   st->breakdown = 0;
+  st->kcols = -1;
+  st->nu = 1.0;
   *vscale0 = beta > 0.0 ? 1.0 / beta : 0.0;
 }
 
 __global__ void gmres_solve_y_kernel(GmresState* st, int k) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const double* H = st->H;
+  // DCGS2 records the usable column count on the device (kcols < 0: the host's k)
+  if (st->kcols >= 0 && st->kcols < k) {
+    for (int i = st->kcols; i < k; ++i) st->y[i] = 0.0;
+    k = st->kcols;
+  }
   for (int i = k - 1; i >= 0; --i) {
     double s = st->g[i];
     for (int l = i + 1; l < k; ++l) s -= H[i + l * kLdH] * st->y[l];
     st->y[i] = s / H[i + i * kLdH];
   }
+}
+
+// ------------------------------------------------------------------------------ DCGS2 Arnoldi
+// Classical Gram-Schmidt with delayed re-orthogonalisation ("DCGS2": the second CGS pass of vector j
+// runs in iteration j+1, fused with the first pass of the next vector, the norm by Pythagoras), so an
+// Arnoldi step streams the basis twice instead of three times: one dots pass (j+2 vectors read) and
+// one update pass (j+2 read, 2 written) against CGS2's 3j+7 vectors.  In exact arithmetic the
+// iterates are those of CGS2 / MGS GMRES [Saad86]; the convergence test uses the
+// once-orthogonalised norm of the newest vector (it differs from the twice-orthogonalised one at
+// rounding level).
+
+// chunk of up to CH basis vectors [i0, i0+cnt): a_l = V_{i0+l}.u, c_l = V_{i0+l}.w; with `first` also
+// sigma = u.u and gamma = u.w.  u = V_j, all values unscaled (finish_a applies the lazy scales).
+template <int CH>
+__global__ void __launch_bounds__(256) dcgs_dots_kernel(BasisPtrs b, int i0, int cnt, int j, int first,
+                                                        const double* __restrict__ w, double* __restrict__ partial,
+                                                        int NT, long long n2, const int* skip) {
+  if (skip_launch(skip)) return;
+  double acc_a[CH], acc_c[CH];
+  double sig = 0.0, gam = 0.0;
+#pragma unroll
+  for (int l = 0; l < CH; ++l) acc_a[l] = acc_c[l] = 0.0;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  const double2* u2 = reinterpret_cast<const double2*>(b.V[j]);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long long)gridDim.x * blockDim.x) {
+    const double2 ww = __ldg(w2 + e);
+    const double2 uu = __ldg(u2 + e);
+    double2 vv[CH];
+#pragma unroll
+    for (int l = 0; l < CH; ++l)
+      if (l < cnt) vv[l] = __ldg(reinterpret_cast<const double2*>(b.V[i0 + l]) + e);
+#pragma unroll
+    for (int l = 0; l < CH; ++l) {
+      if (l < cnt) {
+        acc_a[l] = fma(vv[l].x, uu.x, fma(vv[l].y, uu.y, acc_a[l]));
+        acc_c[l] = fma(vv[l].x, ww.x, fma(vv[l].y, ww.y, acc_c[l]));
+      }
+    }
+    if (first) {
+      sig = fma(uu.x, uu.x, fma(uu.y, uu.y, sig));
+      gam = fma(uu.x, ww.x, fma(uu.y, ww.y, gam));
+    }
+  }
+  // block reduction of 2 cnt (+2) values, fixed order
+  __shared__ double red[8][2 * CH + 2];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int l = 0; l < CH; ++l) {
+    if (l < cnt) {
+      const double sa = warp_sum(acc_a[l]), sc = warp_sum(acc_c[l]);
+      if (lane == 0) { red[wp][l] = sa; red[wp][CH + l] = sc; }
+    }
+  }
+  if (first) {
+    const double ss = warp_sum(sig), sg = warp_sum(gam);
+    if (lane == 0) { red[wp][2 * CH] = ss; red[wp][2 * CH + 1] = sg; }
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  double* out = partial + (long long)blockIdx.x * NT;
+  for (int t = threadIdx.x; t < 2 * CH + 2; t += blockDim.x) {
+    int dst;
+    if (t < CH) dst = t < cnt ? i0 + t : -1;
+    else if (t < 2 * CH) dst = (t - CH) < cnt ? j + i0 + (t - CH) : -1;
+    else dst = first ? 2 * j + (t - 2 * CH) : -1;
+    if (dst < 0) continue;
+    double v = 0.0;
+    for (int k = 0; k < nw; ++k) v += red[k][t];
+    out[dst] = v;
+  }
+}
+
+// chunk [i0, i0+cnt) of the update: q_j += sum cq_i V_i (j > 0), u' += sum cu_i V_i.  The first chunk
+// starts from q_j = cq_j V_j and u' = w + cu_j V_j, later chunks from the partial outputs; the last
+// chunk also writes the partial sums of ||u'||^2.
+template <int CH>
+__global__ void __launch_bounds__(256) dcgs_update_kernel(BasisPtrs b, int i0, int cnt, int j, int first, int last,
+                                                          const GmresState* __restrict__ st,
+                                                          const double* __restrict__ w, double* outq, double* outu,
+                                                          double* __restrict__ partial, long long n2, const int* skip) {
+  if (skip_launch(skip)) return;
+  double cq[CH], cu[CH];
+#pragma unroll
+  for (int l = 0; l < CH; ++l) {
+    cq[l] = l < cnt ? st->cq[i0 + l] : 0.0;
+    cu[l] = l < cnt ? st->cu[i0 + l] : 0.0;
+  }
+  const double cqj = st->cq[j], cuj = st->cu[j];
+  const bool wq = j > 0;
+  double acc[1] = {0.0};
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  double2* q2 = reinterpret_cast<double2*>(outq);
+  double2* u2 = reinterpret_cast<double2*>(outu);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long long)gridDim.x * blockDim.x) {
+    double2 aq, au;
+    if (first) {
+      const double2 vj = q2[e];  // V_j (read before it is overwritten by q_j, same thread)
+      const double2 ww = __ldg(w2 + e);
+      aq = make_double2(cqj * vj.x, cqj * vj.y);
+      au = make_double2(fma(cuj, vj.x, ww.x), fma(cuj, vj.y, ww.y));
+    } else {
+      aq = wq ? q2[e] : make_double2(0.0, 0.0);
+      au = u2[e];
+    }
+    double2 vv[CH];
+#pragma unroll
+    for (int l = 0; l < CH; ++l)
+      if (l < cnt) vv[l] = __ldg(reinterpret_cast<const double2*>(b.V[i0 + l]) + e);
+#pragma unroll
+    for (int l = 0; l < CH; ++l) {
+      if (l < cnt) {
+        aq.x = fma(cq[l], vv[l].x, aq.x);
+        aq.y = fma(cq[l], vv[l].y, aq.y);
+        au.x = fma(cu[l], vv[l].x, au.x);
+        au.y = fma(cu[l], vv[l].y, au.y);
+      }
+    }
+    if (wq) q2[e] = aq;
+    u2[e] = au;
+    if (last) acc[0] = fma(au.x, au.x, fma(au.y, au.y, acc[0]));
+  }
+  if (last) block_reduce_store<1>(acc, 1, partial, nullptr);
+}
+
+// apply the stored rotations 0..j-1 to the column col[0..j+1], then form rotation j; returns the
+// rotated column in R's column j and updates g from gsave[j] (g_j before the rotation)
+__device__ void dcgs_rotate_column(GmresState* st, double* col, int j) {
+  double* R = st->H;
+  for (int i = 0; i < j; ++i) {
+    const double a = col[i], b = col[i + 1];
+    col[i] = st->cs[i] * a + st->sn[i] * b;
+    col[i + 1] = -st->sn[i] * a + st->cs[i] * b;
+  }
+  const double a = col[j], b = col[j + 1];
+  const double den = hypot(a, b);
+  st->cs[j] = den > 0.0 ? a / den : 1.0;
+  st->sn[j] = den > 0.0 ? b / den : 0.0;
+  for (int i = 0; i < j; ++i) R[i + j * kLdH] = col[i];
+  R[j + j * kLdH] = den;
+  R[(j + 1) + j * kLdH] = 0.0;
+  const double gj = st->gsave[j];
+  st->g[j + 1] = -st->sn[j] * gj;
+  st->g[j] = st->cs[j] * gj;
+}
+
+__global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, const double* __restrict__ partial,
+                                                            int nblk, int j, double* vscale, const int* skip) {
+  if (skip_launch(skip)) return;
+  __shared__ double red[2 * 52 + 2];
+  const int NT = 2 * j + 2;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  for (int t = wp; t < NT; t += (int)(blockDim.x >> 5)) {
+    double v = 0.0;
+    for (int bb = lane; bb < nblk; bb += 32) v += partial[(long long)bb * NT + t];
+    v = warp_sum(v);
+    if (lane == 0) red[t] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double* Hr = st->Hraw;
+  const double sj = vscale[j];
+  if (j == 0) {
+    // q_0 = s_0 V_0 is exactly normalised (explicit norm of r_0): one CGS pass, nu = 1
+    const double gam = red[1] * sj;
+    Hr[0] = gam;
+    st->cu[0] = -gam * sj;
+    st->cq[0] = 0.0;
+    st->nu = 1.0;
+    return;
+  }
+  double a[52], c[52], t[52], qtw[52];
+  double ss = 0.0, sc = 0.0;
+  for (int i = 0; i < j; ++i) {
+    a[i] = red[i] * vscale[i] * sj;
+    c[i] = red[j + i] * vscale[i];
+    ss += a[i] * a[i];
+    sc += a[i] * c[i];
+  }
+  const double sig = red[2 * j] * sj * sj, gam = red[2 * j + 1] * sj;
+  const double nu2 = sig - ss;  // ||u - Q a||^2 by Pythagoras (u once-orthogonalised: a = O(eps))
+  const double nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+  st->nu = nu;
+  // column j-1: K q_{j-1} = Q_{j-1} h + nu1 u  and  u = Q_{j-1} a + nu q_j
+  const double nu1 = Hr[j + (j - 1) * kLdH];
+  double col[53];
+  for (int i = 0; i < j; ++i) {
+    Hr[i + (j - 1) * kLdH] += nu1 * a[i];
+    col[i] = Hr[i + (j - 1) * kLdH];
+  }
+  Hr[j + (j - 1) * kLdH] = nu1 * nu;
+  col[j] = nu1 * nu;
+  dcgs_rotate_column(st, col, j - 1);
+  if (nu == 0.0) {
+    // u_j lies in span(Q_{j-1}): column j-1 was exact (lucky breakdown); the update pass becomes a
+    // no-op on V_j and finish_b is skipped; the y solve uses the j corrected columns
+    st->breakdown = 1;
+    st->converged = 1;
+    st->kcols = j;
+    st->relres = fabs(st->g[j]) / st->beta0;
+    for (int i = 0; i <= j; ++i) st->cq[i] = st->cu[i] = 0.0;
+    st->cq[j] = 1.0;
+    return;
+  }
+  // K q_j = (w - Q_j t)/nu with t = Hbar_{0..j, 0..j-1} a  (K Q_{j-1} = Q_j Hbar)
+  for (int l = 0; l <= j; ++l) {
+    double v = 0.0;
+    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) v += Hr[l + i * kLdH] * a[i];
+    t[l] = v;
+  }
+  for (int i = 0; i < j; ++i) qtw[i] = c[i];
+  qtw[j] = (gam - sc) / nu;  // q_j . w
+  for (int l = 0; l <= j; ++l) Hr[l + j * kLdH] = (qtw[l] - t[l]) / nu;  // tentative column j
+  // q_j = (s_j V_j - sum_i a_i s_i V_i)/nu;  nu u_{j+1} = w - (qtw_j/nu) u - sum_i (c_i - qtw_j a_i/nu) q_i
+  const double ej = qtw[j] / nu;
+  for (int i = 0; i < j; ++i) {
+    st->cq[i] = -a[i] * vscale[i] / nu;
+    st->cu[i] = -(c[i] - ej * a[i]) * vscale[i];
+  }
+  st->cq[j] = sj / nu;
+  st->cu[j] = -ej * sj;
+  vscale[j] = 1.0;  // V_j holds q_j after the update pass (which reads cq/cu only)
+}
+
+__global__ void __launch_bounds__(256) dcgs_finish_b_kernel(GmresState* st, const double* __restrict__ pnrm, int nblk,
+                                                            int j, double tol, double* vscale, const int* skip) {
+  if (skip_launch(skip)) return;  // (uniform over the block, before the reduction's barriers)
+  const double nrm2 = block_sum_partials(pnrm, nblk);
+  if (threadIdx.x != 0) return;
+  double* Hr = st->Hraw;
+  const double un = sqrt(nrm2);
+  const double nu = st->nu;
+  Hr[(j + 1) + j * kLdH] = un / nu;  // ||u_{j+1}|| (u' = nu u_{j+1})
+  vscale[j + 1] = un > 0.0 ? 1.0 / un : 0.0;
+  double col[53];
+  for (int i = 0; i <= j + 1; ++i) col[i] = Hr[i + j * kLdH];
+  st->gsave[j] = st->g[j];
+  dcgs_rotate_column(st, col, j);
+  st->relres = fabs(st->g[j + 1]) / st->beta0;
+  st->converged = st->relres <= tol ? 1 : 0;
+  st->breakdown = (un == 0.0) ? 1 : 0;
+  st->kcols = j + 1;
 }
 
 // dense [rows][n_d] <-> padded [rows][P]
@@ -504,6 +752,67 @@ cudaError_t launch_arnoldi_finish(GmresState* st, const double* h1, const double
 cudaError_t launch_gmres_init(GmresState* st, const double* partial_nrm, int nblk, double* vscale0, int first_cycle,
                               cudaStream_t s) {
   gmres_init_kernel<<<1, 256, 0, s>>>(st, partial_nrm, nblk, vscale0, first_cycle);
+  return cudaGetLastError();
+}
+
+template <int CH>
+static void run_dcgs_dots(unsigned g, cudaStream_t s, BasisPtrs b, int i0, int cnt, int j, int first, const double* w,
+                          double* part, int NT, long long n2, const int* skip) {
+  dcgs_dots_kernel<CH><<<g, 256, 0, s>>>(b, i0, cnt, j, first, w, part, NT, n2, skip);
+}
+template <int CH>
+static void run_dcgs_update(unsigned g, cudaStream_t s, BasisPtrs b, int i0, int cnt, int j, int first, int last,
+                            const GmresState* st, const double* w, double* oq, double* ou, double* part,
+                            long long n2, const int* skip) {
+  dcgs_update_kernel<CH><<<g, 256, 0, s>>>(b, i0, cnt, j, first, last, st, w, oq, ou, part, n2, skip);
+}
+#define RSFDE_CH(FN, C, ...)                 \
+  do {                                       \
+    if ((C) <= 4) FN<4>(__VA_ARGS__);        \
+    else if ((C) <= 8) FN<8>(__VA_ARGS__);   \
+    else FN<16>(__VA_ARGS__);                \
+  } while (0)
+
+constexpr int kDcgsChunk = 16;
+
+cudaError_t launch_dcgs_dots(const double* const* V, int j, const double* w, double* partial, long long NP, int nblk,
+                             const int* skip, cudaStream_t s) {
+  if (j < 0 || j + 1 >= kMaxBasis) return cudaErrorInvalidValue;
+  const unsigned g = grid_for(NP / 2, nblk);
+  const BasisPtrs b = make_basis(V, j + 1);
+  const int NT = 2 * j + 2;
+  // chunks of <= 16 basis vectors (u and w are re-read per extra chunk; j < 16 in practice)
+  for (int i0 = 0; i0 == 0 || i0 < j; i0 += kDcgsChunk) {
+    const int cnt = j - i0 < kDcgsChunk ? j - i0 : kDcgsChunk;
+    RSFDE_CH(run_dcgs_dots, cnt, g, s, b, i0, cnt, j, i0 == 0 ? 1 : 0, w, partial, NT, NP / 2, skip);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dcgs_finish_a(GmresState* st, const double* partial, int nblk, int j, double* vscale, const int* skip,
+                                 cudaStream_t s) {
+  dcgs_finish_a_kernel<<<1, 256, 0, s>>>(st, partial, nblk, j, vscale, skip);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dcgs_update(const double* const* V, int j, const GmresState* st, const double* w,
+                               double* partial_nrm, long long NP, int nblk, const int* skip, cudaStream_t s) {
+  if (j < 0 || j + 2 > kMaxBasis) return cudaErrorInvalidValue;
+  const unsigned g = grid_for(NP / 2, nblk);
+  const BasisPtrs b = make_basis(V, j + 2);
+  double* oq = const_cast<double*>(V[j]);
+  double* ou = const_cast<double*>(V[j + 1]);
+  for (int i0 = 0; i0 == 0 || i0 < j; i0 += kDcgsChunk) {
+    const int cnt = j - i0 < kDcgsChunk ? j - i0 : kDcgsChunk;
+    const int last = i0 + kDcgsChunk >= j ? 1 : 0;
+    RSFDE_CH(run_dcgs_update, cnt, g, s, b, i0, cnt, j, i0 == 0 ? 1 : 0, last, st, w, oq, ou, partial_nrm, NP / 2, skip);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dcgs_finish_b(GmresState* st, const double* partial_nrm, int nblk, int j, double tol, double* vscale,
+                                 const int* skip, cudaStream_t s) {
+  dcgs_finish_b_kernel<<<1, 256, 0, s>>>(st, partial_nrm, nblk, j, tol, vscale, skip);
   return cudaGetLastError();
 }
 

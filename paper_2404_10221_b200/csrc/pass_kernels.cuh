@@ -81,16 +81,17 @@ __device__ __forceinline__ void pencil_coords(const PassParams& p, long long idx
 }
 
 __device__ __forceinline__ void pencil_consts(const PassParams& p, int c0, int c1, int c2, double& eP, double& eK,
-                                              long long& eoff, double& cH, double& cP) {
+                                              long long& eoff, double& cH, double& cP, bool want_e = true,
+                                              bool want_spec = true) {
   const int c[3] = {c0 + p.coff[0], c1 + p.coff[1], c2 + p.coff[2]};  // global coordinates
   const Geom& G = p.geo;
   eP = 1.0; eK = 0.0; cH = 1.0; cP = 0.0; eoff = 0;
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
     if (i < G.d && i != p.axis) {
-      if (p.e.g[i]) eP *= __ldg(p.e.g[i] + c[i]);
-      if (p.e.k[i]) eK += __ldg(p.e.k[i] + c[i]);
-      if (p.spec.lamH[i]) {
+      if (want_e && p.e.g[i]) eP *= __ldg(p.e.g[i] + c[i]);
+      if (want_e && p.e.k[i]) eK += __ldg(p.e.k[i] + c[i]);
+      if (want_spec && p.spec.lamH[i]) {
         cH *= __ldg(p.spec.lamH[i] + c[i]);
         cP += __ldg(p.spec.tq[i] + c[i]);
       }
@@ -147,13 +148,14 @@ __device__ __forceinline__ PairCtx make_pair(const PassParams& p, long long pair
   return pc;
 }
 
-__device__ __forceinline__ PencilConsts make_consts(const PassParams& p, const PairCtx& pc) {
+__device__ __forceinline__ PencilConsts make_consts(const PassParams& p, const PairCtx& pc, bool want_e = true,
+                                                    bool want_spec = true) {
   PencilConsts k;
   int a0, a1, a2, b0, b1, b2;
   pencil_coords(p, pc.pen_p, a0, a1, a2);
   pencil_coords(p, pc.pen_q, b0, b1, b2);
-  pencil_consts(p, a0, a1, a2, k.eP_p, k.eK_p, k.eoff_p, k.cH_p, k.cP_p);
-  pencil_consts(p, b0, b1, b2, k.eP_q, k.eK_q, k.eoff_q, k.cH_q, k.cP_q);
+  pencil_consts(p, a0, a1, a2, k.eP_p, k.eK_p, k.eoff_p, k.cH_p, k.cP_p, want_e, want_spec);
+  pencil_consts(p, b0, b1, b2, k.eP_q, k.eK_q, k.eoff_q, k.cH_q, k.cP_q, want_e, want_spec);
   return k;
 }
 
@@ -344,6 +346,7 @@ __device__ __forceinline__ void odd_extend(double2 (&v)[T::E], double2* buf, int
 template <class T, int MODE>
 __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassParams p) {
   extern __shared__ double2 smem[];
+  if (skip_launch(p.skip)) return;  // speculative launch after convergence (uniform over the grid)
   constexpr int E = T::E, G = T::G, L = T::L, N = T::N, GROUPS = T::GROUPS;
   constexpr bool OPER = MODE <= MODE_OPER_SPEC_LAST;
   constexpr bool SPECTRAL = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST || MODE >= MODE_DST;

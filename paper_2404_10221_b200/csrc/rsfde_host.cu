@@ -208,6 +208,7 @@ PassParams rsfde_axis_params(const rsfde_ctx* c, int axis) {
   p.dst_scale = std::sqrt(2.0 / (double)p.N);
   p.ycoef = 1.0;
   p.flags = c->pass_flags;
+  p.skip = c->skip;
   p.chat = c->d_chat[axis];
   p.tw = c->d_tw[axis];
   p.lamH = c->d_lamH[axis];
@@ -430,6 +431,61 @@ static rsfde_status read_flags(rsfde_ctx* c, Flags* f, cudaStream_t s) {
   return RSFDE_OK;
 }
 
+// One GMRES cycle of DCGS2 Arnoldi steps (krylov_kernels.cu) after gmres_init.  The host runs one
+// iteration ahead of the flags: iteration j+1 is enqueued before the convergence flag of iteration j is
+// read (an async copy into pinned memory + an event), and every kernel of a step returns at once when
+// the device flags say the previous step converged (PassParams::skip), so the GPU never idles on the
+// host round trip.  Returns the number of Arnoldi steps done in *k and the last flags in *fl.
+static rsfde_status dcgs_cycle(rsfde_ctx* c, int form, int m, int restart, int max_iters, int fixed, double tol,
+                               int total, cudaStream_t s, int* k, Flags* fl) {
+  const long long NP = c->geo.NP;
+  const int nb = reduction_blocks(NP, c->nblk);
+  const double vb = 8.0 * (double)NP;
+  const int* skip = reinterpret_cast<const int*>(c->d_state);  // converged, breakdown
+  static const bool no_spec = getenv("RSFDE_NO_SPEC") != nullptr;
+  const int lag = (c->profiling || no_spec) ? 0 : 1;
+  for (int i = 0; i < 2; ++i)
+    if (!c->flag_ev[i]) CK(cudaEventCreateWithFlags(&c->flag_ev[i], cudaEventDisableTiming), "event");
+  Flags* slots = reinterpret_cast<Flags*>(c->h_flags);
+  int jl = 0, jr = 0;
+  while (true) {
+    const bool can_launch = jl < restart && total + jl < max_iters && !(fixed > 0 && total + jl >= fixed);
+    if (can_launch) {
+      const int j = jl;
+      const double* const* Vp = (const double* const*)c->V.data();
+      c->skip = j > 0 ? skip : nullptr;
+      const rsfde_status st = apply_K(c, form, m, c->V[j], c->d_vscale + j, c->Z, s);
+      c->skip = nullptr;
+      TRY(st);
+      const int* sk = j > 0 ? skip : nullptr;
+      // one dots pass (j+2 vectors) + one update pass (j+2 read, 2 written)
+      LAUNCH(PC_DOTS, vb * (j + 2), launch_dcgs_dots(Vp, j, c->Z, c->d_part, NP, c->nblk, sk, s), "dcgs dots");
+      CKL(launch_dcgs_finish_a(c->d_state, c->d_part, nb, j, c->d_vscale, sk, s), "dcgs finish a");
+      LAUNCH(PC_UPD, vb * (j + 2 + (j > 0 ? 2 : 1)),
+             launch_dcgs_update(Vp, j, c->d_state, c->Z, c->d_nrm, NP, c->nblk, sk, s), "dcgs update");
+      CKL(launch_dcgs_finish_b(c->d_state, c->d_nrm, nb, j, tol, c->d_vscale, sk, s), "dcgs finish b");
+      CK(cudaMemcpyAsync(&slots[j & 1], c->d_state, sizeof(Flags), cudaMemcpyDeviceToHost, s), "flags copy");
+      CK(cudaEventRecord(c->flag_ev[j & 1], s), "flags event");
+      ++jl;
+    }
+    if (jr < jl - (can_launch ? lag : 0)) {
+      CK(cudaEventSynchronize(c->flag_ev[jr & 1]), "flags wait");
+      memcpy(fl, &slots[jr & 1], sizeof(Flags));
+      if (c->profiling) {
+        CK(cudaStreamSynchronize(s), "stream sync");
+        prof_collect(c);
+      }
+      ++jr;
+      const bool stop = fixed > 0 ? total + jr >= fixed : fl->converged != 0;
+      if (stop || fl->breakdown || total + jr >= max_iters || jr == restart) break;
+    } else if (!can_launch) {
+      break;
+    }
+  }
+  *k = jr;
+  return RSFDE_OK;
+}
+
 // GMRES on K x = P^{-1} b with x = c->X on entry (x0) and exit.
 // mode_fast: first-cycle r0 = P_hat^{-1}(H FH - 2 S_alpha x0) with FH = H^{-1} tau F (valid iff
 // x0 = u^{(m)}: b - A u = tau F - 2 S_alpha u, Eq.(tls)); later cycles use b (computed on demand).
@@ -488,7 +544,11 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
       break;
     }
     int k = 0;
-    for (int j = 0; j < restart; ++j) {
+    if (c->ortho == ORTHO_DCGS2) {
+      TRY(dcgs_cycle(c, form, m, restart, max_iters, fixed, tol, total, s, &k, &fl));
+      total += k;
+    }
+    for (int j = 0; j < restart && c->ortho != ORTHO_DCGS2; ++j) {
       const int J = j + 1;
       TRY(apply_K(c, form, m, c->V[j], c->d_vscale + j, c->Z, s));
       const double* const* Vp = (const double* const*)c->V.data();
@@ -655,6 +715,8 @@ void rsfde_destroy(rsfde_ctx* c) {
   if (c->h_flags) cudaFreeHost(c->h_flags);
   prof_collect(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->flag_ev)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -705,6 +767,11 @@ rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void*
   c->tau = p->tau_t;
   c->M = p->M;
   if (getenv("RSFDE_NO_PIPE")) c->pass_flags |= PASS_FLAG_NO_PIPE;
+  {
+    // Arnoldi orthogonalisation: DCGS2 (default) or the three-pass CGS2 (RSFDE_ORTHO=cgs2)
+    const char* o = getenv("RSFDE_ORTHO");
+    c->ortho = (o && !strcmp(o, "cgs2")) ? ORTHO_CGS2 : ORTHO_DCGS2;
+  }
   c->geo.d = c->d;
   for (int i = 0; i < 3; ++i) c->geo.n[i] = c->n[i];
   c->geo.P = c->n[c->d - 1] + 1;
@@ -768,7 +835,7 @@ rsfde_status rsfde_setup_internal(rsfde_ctx** out, const rsfde_problem* p, void*
   if ((st = dalloc(c, (void**)&c->d_vscale, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_h1, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_h2, 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
-  if ((st = dalloc(c, (void**)&c->d_part, (size_t)c->nblk * 64 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
+  if ((st = dalloc(c, (void**)&c->d_part, (size_t)c->nblk * 128 * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_nrm, (size_t)c->nblk * sizeof(double))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if ((st = dalloc(c, (void**)&c->d_state, sizeof(GmresState))) != RSFDE_OK) return setup_fail(c, st, nullptr);
   if (cudaMallocHost(&c->h_flags, 64) != cudaSuccess) return setup_fail(c, RSFDE_E_NOMEM, "cudaMallocHost");

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long ntiles = CT ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
   const int jobs_per_tile = OPER ? (p.xmode == X_ZERO ? 1 : 2) : 1;
+  if (skip_launch(p.skip)) return;  // speculative launch after convergence (uniform over the grid)
   if (threadIdx.x == 0) {
     mbar_init(&full_bar, 1);
     mbar_init(&empty_bar, CW);
@@ -240,6 +241,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   const double rsh = rs * hs;
   // the lazy basis scale rs of R folds into eta (T R enters y only as eta T R) and into the C factor
   const double hc0s = p.hc0 * hs, hc1s = p.hc1 * hs, etas = p.eta * rsh, crs = OPER ? rsh : hs;
+  const double etas_y = (E == G) ? -etas : etas;
   long long job = 0;
   int tcount = 0;
   (void)tcount;
@@ -251,6 +253,10 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     const bool active = pair < p.npairs;
     const PairCtx pc = make_pair(p, active ? pair : 0, active);
     if (g == 0) tvalid[w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
+    // per-pencil constants of e(x,t): their table loads are issued here, at the tile start, so that
+    // their latency hides behind the first FFT (not in the last-axis kernel, where the live
+    // registers would spill; the last-axis spectrum constants are loaded where they are used)
+    const PencilConsts kc0 = (OPER && !LAST && p.xmode == X_E_TIMES_R) ? make_consts(p, pc, true, false) : PencilConsts{};
     double2 v[E];
     TTRACE(0)
     // ---- job 0: primary input
@@ -294,16 +300,12 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
       // layout exactly like fft_inv.
       int ph;
       asm volatile("mov.b32 %0, %1;" : "=r"(ph) : "r"(ph0));
-      const unsigned long long cmsk = (ph == 1) ? 0x8000000000000000ull : 0ull;
       if (!(RSFDE_TILE_SKIP & 1)) {
         if constexpr (E == G) {
-#pragma unroll
-          for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
+          // phase 1 (the convolution's inverse FFT) is conj(FFT(conj(.))): the input conj is folded
+          // into the spectrum scaling of phase 0 and the output conj into the stencil of phase 1
           fft_fwd<E, G>(v, buf, g, p.tw);
-#pragma unroll
-          for (int i = 0; i < E; ++i) v[i].y = sgnx(v[i].y, cmsk);
         } else {
-          (void)cmsk;
           T::fft(v, buf, g, p.tw, ph == 1);  // E = R G: forward and inverse differ in layout
         }
       }
@@ -357,12 +359,21 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           }
         }
         TTRACE(9)
+        if constexpr (E == G) {
+          // scaled conj spectrum: the inverse FFT of phase 1 runs as a forward FFT (see above)
 #pragma unroll
-        for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
+          for (int r = 0; r < E; ++r) {
+            const double ch = __ldg(p.chat + T::rowk(g, r));
+            v[r] = make_double2(v[r].x * ch, -v[r].y * ch);
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
+        }
       } else if (OPER && ph == 1) {
         // X channel from the stage (job 1) into the pair buffer (x = X, or e o R), then
         // y = H X + eta T R on j = g + G m with the stencil neighbours from the buffer
-        const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
+        const PencilConsts kc = (LAST && p.xmode == X_E_TIMES_R) ? make_consts(p, pc, true, false) : kc0;
         if (p.xmode != X_ZERO) mbar_wait(&full_bar, (unsigned)(job & 1));
         TTRACE(11)
         __syncwarp();
@@ -401,8 +412,9 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           double2 y = make_double2(0.0, 0.0);
           if (j >= 1 && j <= p.n) {
             const double2 xl = buf[j - 1], x0 = buf[j], xn = buf[j + 1];
+            // (E == G: phase 1 returned conj(T R), so the imaginary part enters with -eta)
             y.x = fma(hc0s, x0.x, fma(hc1s, xl.x + xn.x, etas * v[m].x));
-            y.y = fma(hc0s, x0.y, fma(hc1s, xl.y + xn.y, etas * v[m].y));
+            y.y = fma(hc0s, x0.y, fma(hc1s, xl.y + xn.y, etas_y * v[m].y));
           }
           v[m] = y;
         }
@@ -411,7 +423,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
       } else if (ph == 2 && LAST) {
         // S y (row layout, k = g + G r for r < E/2) into the pair buffer, then Lambda^{-1} in a rolled
         // loop over the same k (small code: the spectrum kinds are a runtime switch)
-        const PencilConsts kc = make_consts(p, pc);
+        const PencilConsts ks = make_consts(p, pc, false, true);
         const Spec& S = p.spec;
         __syncwarp();
 #pragma unroll
@@ -423,8 +435,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         // Lambda = (ebar + cP + tq_k) cH lh_k (P_hat) | (ebar + cP + tq_k) (P_alpha) | cH lh_k (H):
         // one fast reciprocal per value instead of an IEEE division
         const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
-        const double icHp = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_p) * hs;  // (hs of the inverse DST)
-        const double icHq = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / kc.cH_q) * hs;
+        const double icHp = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / ks.cH_p) * hs;  // (hs of the inverse DST)
+        const double icHq = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / ks.cH_q) * hs;
         if (fast && !e_tab) {
           // unrolled: the 16 values are independent (a rolled loop serialises the latencies)
 #pragma unroll
@@ -437,8 +449,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
               double lp = 1.0, lq = 1.0;
               if (S.kind != SPEC_HINV) {
                 const double tq = e_ka[k - 1];
-                lp = S.ebar + kc.cP_p + tq;
-                lq = S.ebar + kc.cP_q + tq;
+                lp = S.ebar + ks.cP_p + tq;
+                lq = S.ebar + ks.cP_q + tq;
               }
               wv.x = pc.vp ? z.x * (rcp_nr(lp * lh) * icHp) : 0.0;
               wv.y = pc.vq ? z.y * (rcp_nr(lq * lh) * icHq) : 0.0;
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             double2 wv = make_double2(0.0, 0.0);
             if (k >= 1) {
               const double2 z = buf[k];
-              const double2 lam = spec_pair(p, kc, k);
+              const double2 lam = spec_pair(p, ks, k);
               wv.x = pc.vp ? (z.x * hs) / lam.x : 0.0;
               wv.y = pc.vq ? (z.y * hs) / lam.y : 0.0;
             }

@@ -74,7 +74,9 @@ def test_full_size_operator_parity(name):
 # ----------------------------------------------------------------------------- marches
 def _march_gpu(prob, steps, cfg_kw=None):
     S = _solver(prob)
-    cfg = S.cfg(restart=prob.restart, tol=prob.tol, **(cfg_kw or {}))
+    kw = {"restart": prob.restart, "tol": prob.tol}
+    kw.update(cfg_kw or {})
+    cfg = S.cfg(**kw)
     u = _dev(prob.psi_interior())
     if prob.source_static:
         F = S.compact_source(_dev(prob.f_closed(prob.t_half(0))))

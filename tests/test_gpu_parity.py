@@ -353,3 +353,32 @@ def test_tile128_matvec_and_precond_parity(kind, shape, monkeypatch, cache):
     monkeypatch.setenv("RSFDE_TILE128", "1")
     test_matvec_parity(cache, kind, shape, 0)
     test_precond_parity(cache, kind, shape)
+
+
+# ----------------------------------------------------------------------- Arnoldi variants
+@pytest.mark.parametrize("name", ["c5s", "ex2", "c2s"])
+def test_dcgs2_matches_cgs2_and_oracle(name, monkeypatch):
+    # the default DCGS2 Arnoldi (delayed re-orthogonalisation, one dots + one update pass) and the
+    # three-pass CGS2 (RSFDE_ORTHO=cgs2) are the same Krylov process: equal iteration counts and
+    # solutions to rounding; the speculative one-ahead launches (RSFDE_NO_SPEC=1 disables them) do
+    # not change a single bit
+    prob = {"c5s": lambda: I.config_c5(M=4, nn=(31, 15, 63)),
+            "ex2": lambda: I.example(2, 31, 8, (1.5, 1.7)),
+            "c2s": lambda: I.config_c2(n=63, M=6)}[name]()
+    u_d, r_d = _march(prob)
+    monkeypatch.setenv("RSFDE_NO_SPEC", "1")
+    u_ns, r_ns = _march(prob)
+    monkeypatch.delenv("RSFDE_NO_SPEC")
+    assert r_ns["iters"] == r_d["iters"] and np.array_equal(u_ns, u_d)
+    monkeypatch.setenv("RSFDE_ORTHO", "cgs2")
+    u_c, r_c = _march(prob)
+    monkeypatch.delenv("RSFDE_ORTHO")
+    assert max(abs(a - b) for a, b in zip(r_d["iters"], r_c["iters"])) <= 1
+    if r_d["iters"] == r_c["iters"]:
+        assert relerr(u_d, u_c) < 1e-11
+    Fst = scheme.source_F(prob, 0) if prob.source_static else None
+    uo, ro, _ = scheme.solve(prob, F_static=Fst)
+    assert max(abs(a - b) for a, b in zip(r_d["iters"], ro.iters)) <= 1
+    if r_d["iters"] != ro.iters:
+        uo, ro, _ = scheme.solve(prob, F_static=Fst, fixed_iters=r_d["iters"])
+    assert relerr(u_d, uo) < 1e-9
