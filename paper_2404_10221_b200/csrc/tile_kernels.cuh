@@ -29,6 +29,9 @@ namespace rsfde {
 #ifndef RSFDE_TILE_SKIP
 #define RSFDE_TILE_SKIP 0
 #endif
+#ifndef RSFDE_TILE_COOP_STORES  // strided axes: stage outputs in shared memory, store whole tile rows cooperatively
+#define RSFDE_TILE_COOP_STORES 1   // (0: 16-byte pieces straight from registers -- measured 17 % slower at 511^3)
+#endif
 #ifndef RSFDE_TILE_TRACE  // experiments only: per-tile clock64 stamps of warp 0 of every CTA
 #define RSFDE_TILE_TRACE 0
 #endif
@@ -81,15 +84,18 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// The suspend-time hint lets a waiting warp sleep in the barrier unit until the phase completes
+// instead of re-issuing try_wait: the spinning producer warp otherwise took ~7 % of the issue slots
+// of its sub-partition from the compute warp beside it (ncu, profiles/r01_ncu_tile_final_summary.txt).
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
+      "r"(phase), "r"(1000000u)
       : "memory");
 }
 template <int CW>
@@ -169,6 +175,10 @@ template <int MODE, class T, int TP, bool CT>
 __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg<TP * T::G / 32>::kCtasPerSm)
     tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmX) {
   constexpr int E = T::E, G = T::G, L = T::L, N = T::N, NH = T::N;
+  // the pencil length along the pass axis is fixed by the FFT length (p.n == N - 1, checked by the
+  // launcher): compile-time bounds turn the per-element range tests into predicates and let the
+  // compiler schedule the unrolled plumbing loops freely
+  constexpr int kN = N - 1;
   constexpr int PPW = 32 / G;           // pencil pairs per compute warp
   constexpr int CW = TP / PPW;          // compute warps
   constexpr int kComputeThreads = 32 * CW;
@@ -218,8 +228,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     const double* ga = p.e.g[p.axis];
     const double* ka = p.e.k[p.axis];
     for (int j = threadIdx.x; j < N; j += kComputeThreads) {
-      e_ga[j] = (ga && j < p.n) ? __ldg(ga + j) : 1.0;
-      e_ka[j] = (ka && j < p.n) ? __ldg(ka + j) : 0.0;
+      e_ga[j] = (ga && j < kN) ? __ldg(ga + j) : 1.0;
+      e_ka[j] = (ka && j < kN) ? __ldg(ka + j) : 0.0;
     }
     compute_bar<CW>();
   }
@@ -227,8 +237,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     const double* lh = p.spec.lamH[p.axis];
     const double* tq = p.spec.tq[p.axis];
     for (int j = threadIdx.x; j < N; j += kComputeThreads) {
-      e_ga[j] = (lh && j < p.n) ? __ldg(lh + j) : 1.0;
-      e_ka[j] = (tq && j < p.n) ? __ldg(tq + j) : 0.0;
+      e_ga[j] = (lh && j < kN) ? __ldg(lh + j) : 1.0;
+      e_ka[j] = (tq && j < kN) ? __ldg(tq + j) : 0.0;
     }
     compute_bar<CW>();
   }
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
       for (int m = 0; m < E; ++m) {
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
-        if (m < E / 2 && j >= 1 && j <= p.n) {
+        if (m < E / 2 && j >= 1 && j <= kN) {
           r = stage_pair<TP, NH, CT>(p, stage, w, j);  // raw R (rs folded into eta and the C factor)
           r = make_double2(pc.vp ? r.x : 0.0, pc.vq ? r.y : 0.0);
         }
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
       for (int m = 0; m < E / 2; ++m) {
         const int j = g + G * m;
         double2 r = make_double2(0.0, 0.0);
-        if (j >= 1 && j <= p.n) {
+        if (j >= 1 && j <= kN) {
           r = stage_pair<TP, NH, CT>(p, stage, w, j);
           r = make_double2(pc.vp ? rsh * r.x : 0.0, pc.vq ? rsh * r.y : 0.0);
         }
@@ -326,6 +336,17 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             const double f = (k >= 1) ? crs * __ldg(p.lamH + k - 1) : 0.0;
             cv[i++] = make_double2(-(v[r].y - zm.y) * f, (v[r].x - zm.x) * f);
           }
+          if (!RSFDE_TILE_COOP_STORES) {
+            // store C straight from registers: 16-byte (pencil pair) pieces per row on strided axes
+            // (the neighbouring pairs' warps fill the rest of each row piece at the same time; L2
+            // merges the sectors), coalesced 8-byte elements on the contiguous axis
+#pragma unroll
+            for (int r = 0, i = 0; r < E; ++r) {
+              if (!T::lower(r)) continue;
+              if (!(RSFDE_TILE_SKIP & 2)) st_pair(p, p.C, pc, T::rowk(g, r), cv[i]);
+              ++i;
+            }
+          } else {
           __syncwarp();
 #pragma unroll
           for (int r = 0, i = 0; r < E; ++r) {
@@ -335,7 +356,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           // store C
           if (CT) {
             __syncwarp();
-            for (int j = g + 1; j <= p.n; j += G) {
+            for (int j = g + 1; j <= kN; j += G) {
               const double2 c = buf[oswz(j, w)];
               if (RSFDE_TILE_SKIP & 2) continue;
               if (pc.vp) p.C[pc.off_p + j - 1] = c.x;
@@ -345,7 +366,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           } else {
             compute_bar<CW>();
             const long long base = tile_base<TP, NH, CT>(p, t);
-            for (int e = threadIdx.x; e < p.n * kTilePairs; e += kComputeThreads) {
+            for (int e = threadIdx.x; e < kN * kTilePairs; e += kComputeThreads) {
               const int row = e / kTilePairs, q = e % kTilePairs;
               const double2 c = bufs[q * L + oswz(row + 1, q)];
               const int vm = tvalid[q];
@@ -357,6 +378,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             }
             compute_bar<CW>();
           }
+          }  // RSFDE_TILE_COOP_STORES
         }
         TTRACE(9)
         if constexpr (E == G) {
@@ -381,7 +403,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         for (int m = 0; m < E / 2; ++m) {
           const int j = g + G * m;
           double2 x = make_double2(0.0, 0.0);
-          if (p.xmode != X_ZERO && j >= 1 && j <= p.n) {
+          if (p.xmode != X_ZERO && j >= 1 && j <= kN) {
             x = stage_pair<TP, NH, CT>(p, stage, w, j);
             if (p.xmode == X_E_TIMES_R) {
               double2 e;
@@ -410,7 +432,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         for (int m = 0; m < E / 2; ++m) {
           const int j = g + G * m;
           double2 y = make_double2(0.0, 0.0);
-          if (j >= 1 && j <= p.n) {
+          if (j >= 1 && j <= kN) {
             const double2 xl = buf[j - 1], x0 = buf[j], xn = buf[j + 1];
             // (E == G: phase 1 returned conj(T R), so the imaginary part enters with -eta)
             y.x = fma(hc0s, x0.x, fma(hc1s, xl.x + xn.x, etas * v[m].x));
@@ -485,6 +507,13 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         }
       } else {
         // final DST (row layout) -> Y
+        if (!RSFDE_TILE_COOP_STORES) {
+#pragma unroll
+          for (int r = 0; r < E; ++r) {
+            if (!T::lower(r)) continue;
+            if (!(RSFDE_TILE_SKIP & 2)) st_pair(p, p.Y, pc, T::rowk(g, r), make_double2(-v[r].y, v[r].x));
+          }
+        } else {
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < E; ++r) {
@@ -493,7 +522,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         }
         if (CT) {
           __syncwarp();
-          for (int j = g + 1; j <= p.n; j += G) {
+          for (int j = g + 1; j <= kN; j += G) {
             const double2 yv = buf[oswz(j, w)];
             if (RSFDE_TILE_SKIP & 2) continue;
             if (pc.vp) p.Y[pc.off_p + j - 1] = yv.x;
@@ -503,7 +532,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         } else {
           compute_bar<CW>();
           const long long base = tile_base<TP, NH, CT>(p, t);
-          for (int e = threadIdx.x; e < p.n * kTilePairs; e += kComputeThreads) {
+          for (int e = threadIdx.x; e < kN * kTilePairs; e += kComputeThreads) {
             const int row = e / kTilePairs, q = e % kTilePairs;
             const int vm = tvalid[q];
             if (!(vm & 1)) continue;
@@ -515,6 +544,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           }
           compute_bar<CW>();
         }
+        }  // RSFDE_TILE_COOP_STORES
       }
     }
     TTRACE(6)
@@ -566,6 +596,7 @@ template <int MODE, class T, int TP, bool CT>
 cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
   constexpr int NH = T::N, CW = TP * T::G / 32;
   RSFDE_TILE_CONSTS
+  if (p.n != T::N - 1) return cudaErrorInvalidValue;
   constexpr int kTileThreads = TileCfg<CW>::kTileThreads, kCtasPerSm = TileCfg<CW>::kCtasPerSm;
   constexpr bool OPER = MODE == MODE_OPER_SPEC || MODE == MODE_OPER_SPEC_LAST;
   const size_t smem = (size_t)kTilePairs * T::L * sizeof(double2) + kStageBytes + 1024;  // + alignment slack
