@@ -619,7 +619,10 @@ cudaError_t launch_tile_ct(const PassParams& p, cudaStream_t s) {
   if (err == cudaSuccess && (!OPER || p.xmode == X_INPUT)) err = tile_tensor_map<TP, NH>(p, p.X, &tmX);
   if (err != cudaSuccess) return err;
   const long long ntiles = p.contiguous ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
-  const long long blocks = ntiles < (long long)kCtasPerSm * sms ? ntiles : (long long)kCtasPerSm * sms;
+  // (experiments: RSFDE_TILE_CTAS overrides the resident CTAs per SM of the persistent grid)
+  static const int ctas_env = getenv("RSFDE_TILE_CTAS") ? atoi(getenv("RSFDE_TILE_CTAS")) : 0;
+  const int cps = ctas_env > 0 ? ctas_env : kCtasPerSm;
+  const long long blocks = ntiles < (long long)cps * sms ? ntiles : (long long)cps * sms;
   tile_kernel<MODE, T, TP, CT><<<(unsigned)blocks, kTileThreads, smem, s>>>(p, tmR, tmX);
   err = cudaGetLastError();
   if (err != cudaSuccess && getenv("RSFDE_DEBUG")) {
