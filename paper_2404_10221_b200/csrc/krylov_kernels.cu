@@ -291,7 +291,7 @@ __global__ void gmres_solve_y_kernel(GmresState* st, int k) {
 // chunk of up to CH basis vectors [i0, i0+cnt): a_l = V_{i0+l}.u, c_l = V_{i0+l}.w; with `first` also
 // sigma = u.u and gamma = u.w.  u = V_j, all values unscaled (finish_a applies the lazy scales).
 template <int CH>
-__global__ void __launch_bounds__(256) dcgs_dots_kernel(BasisPtrs b, int i0, int cnt, int j, int first,
+__global__ void __launch_bounds__(256, 2) dcgs_dots_kernel(BasisPtrs b, int i0, int cnt, int j, int first,
                                                         const double* __restrict__ w, double* __restrict__ partial,
                                                         int NT, long long n2, const int* skip) {
   if (skip_launch(skip)) return;
@@ -301,23 +301,34 @@ __global__ void __launch_bounds__(256) dcgs_dots_kernel(BasisPtrs b, int i0, int
   for (int l = 0; l < CH; ++l) acc_a[l] = acc_c[l] = 0.0;
   const double2* w2 = reinterpret_cast<const double2*>(w);
   const double2* u2 = reinterpret_cast<const double2*>(b.V[j]);
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long long)gridDim.x * blockDim.x) {
-    const double2 ww = __ldg(w2 + e);
-    const double2 uu = __ldg(u2 + e);
-    double2 vv[CH];
+  // two grid-stride elements per iteration: all loads of both first (twice the bytes in flight)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += 2 * stride) {
+    const bool two = e0 + stride < n2;
+    double2 ww[2], uu[2], vv[2][CH];
 #pragma unroll
-    for (int l = 0; l < CH; ++l)
-      if (l < cnt) vv[l] = __ldg(reinterpret_cast<const double2*>(b.V[i0 + l]) + e);
+    for (int h = 0; h < 2; ++h) {
+      const long long e = e0 + h * stride;
+      const bool ok = h == 0 || two;
+      ww[h] = ok ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+      uu[h] = ok ? __ldg(u2 + e) : make_double2(0.0, 0.0);
 #pragma unroll
-    for (int l = 0; l < CH; ++l) {
-      if (l < cnt) {
-        acc_a[l] = fma(vv[l].x, uu.x, fma(vv[l].y, uu.y, acc_a[l]));
-        acc_c[l] = fma(vv[l].x, ww.x, fma(vv[l].y, ww.y, acc_c[l]));
-      }
+      for (int l = 0; l < CH; ++l)
+        if (l < cnt) vv[h][l] = ok ? __ldg(reinterpret_cast<const double2*>(b.V[i0 + l]) + e) : make_double2(0.0, 0.0);
     }
-    if (first) {
-      sig = fma(uu.x, uu.x, fma(uu.y, uu.y, sig));
-      gam = fma(uu.x, ww.x, fma(uu.y, ww.y, gam));
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int l = 0; l < CH; ++l) {
+        if (l < cnt) {
+          acc_a[l] = fma(vv[h][l].x, uu[h].x, fma(vv[h][l].y, uu[h].y, acc_a[l]));
+          acc_c[l] = fma(vv[h][l].x, ww[h].x, fma(vv[h][l].y, ww[h].y, acc_c[l]));
+        }
+      }
+      if (first) {
+        sig = fma(uu[h].x, uu[h].x, fma(uu[h].y, uu[h].y, sig));
+        gam = fma(uu[h].x, ww[h].x, fma(uu[h].y, ww[h].y, gam));
+      }
     }
   }
   // block reduction of 2 cnt (+2) values, fixed order
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(256) dcgs_dots_kernel(BasisPtrs b, int i0, int
 // starts from q_j = cq_j V_j and u' = w + cu_j V_j, later chunks from the partial outputs; the last
 // chunk also writes the partial sums of ||u'||^2.
 template <int CH>
-__global__ void __launch_bounds__(256) dcgs_update_kernel(BasisPtrs b, int i0, int cnt, int j, int first, int last,
+__global__ void __launch_bounds__(256, 2) dcgs_update_kernel(BasisPtrs b, int i0, int cnt, int j, int first, int last,
                                                           const GmresState* __restrict__ st,
                                                           const double* __restrict__ w, double* outq, double* outu,
                                                           double* __restrict__ partial, long long n2, const int* skip) {
@@ -370,33 +381,47 @@ __global__ void __launch_bounds__(256) dcgs_update_kernel(BasisPtrs b, int i0, i
   const double2* w2 = reinterpret_cast<const double2*>(w);
   double2* q2 = reinterpret_cast<double2*>(outq);
   double2* u2 = reinterpret_cast<double2*>(outu);
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += (long long)gridDim.x * blockDim.x) {
-    double2 aq, au;
-    if (first) {
-      const double2 vj = q2[e];  // V_j (read before it is overwritten by q_j, same thread)
-      const double2 ww = __ldg(w2 + e);
-      aq = make_double2(cqj * vj.x, cqj * vj.y);
-      au = make_double2(fma(cuj, vj.x, ww.x), fma(cuj, vj.y, ww.y));
-    } else {
-      aq = wq ? q2[e] : make_double2(0.0, 0.0);
-      au = u2[e];
+  // two grid-stride elements per iteration: all loads of both first (twice the bytes in flight)
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += 2 * stride) {
+    const bool two = e0 + stride < n2;
+    double2 aq[2], au[2], vv[2][CH];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long e = e0 + h * stride;
+      const bool ok = h == 0 || two;
+      if (first) {
+        // V_j is read before it is overwritten by q_j (same thread, same element)
+        const double2 vj = ok ? q2[e] : make_double2(0.0, 0.0);
+        const double2 ww = ok ? __ldg(w2 + e) : make_double2(0.0, 0.0);
+        aq[h] = make_double2(cqj * vj.x, cqj * vj.y);
+        au[h] = make_double2(fma(cuj, vj.x, ww.x), fma(cuj, vj.y, ww.y));
+      } else {
+        aq[h] = (wq && ok) ? q2[e] : make_double2(0.0, 0.0);
+        au[h] = ok ? u2[e] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int l = 0; l < CH; ++l)
+        if (l < cnt) vv[h][l] = ok ? __ldg(reinterpret_cast<const double2*>(b.V[i0 + l]) + e) : make_double2(0.0, 0.0);
     }
-    double2 vv[CH];
 #pragma unroll
-    for (int l = 0; l < CH; ++l)
-      if (l < cnt) vv[l] = __ldg(reinterpret_cast<const double2*>(b.V[i0 + l]) + e);
+    for (int h = 0; h < 2; ++h) {
+      const long long e = e0 + h * stride;
 #pragma unroll
-    for (int l = 0; l < CH; ++l) {
-      if (l < cnt) {
-        aq.x = fma(cq[l], vv[l].x, aq.x);
-        aq.y = fma(cq[l], vv[l].y, aq.y);
-        au.x = fma(cu[l], vv[l].x, au.x);
-        au.y = fma(cu[l], vv[l].y, au.y);
+      for (int l = 0; l < CH; ++l) {
+        if (l < cnt) {
+          aq[h].x = fma(cq[l], vv[h][l].x, aq[h].x);
+          aq[h].y = fma(cq[l], vv[h][l].y, aq[h].y);
+          au[h].x = fma(cu[l], vv[h][l].x, au[h].x);
+          au[h].y = fma(cu[l], vv[h][l].y, au[h].y);
+        }
+      }
+      if (h == 0 || two) {
+        if (wq) q2[e] = aq[h];
+        u2[e] = au[h];
+        if (last) acc[0] = fma(au[h].x, au[h].x, fma(au[h].y, au[h].y, acc[0]));
       }
     }
-    if (wq) q2[e] = aq;
-    u2[e] = au;
-    if (last) acc[0] = fma(au.x, au.x, fma(au.y, au.y, acc[0]));
   }
   if (last) block_reduce_store<1>(acc, 1, partial, nullptr);
 }
@@ -768,12 +793,14 @@ static void run_dcgs_update(unsigned g, cudaStream_t s, BasisPtrs b, int i0, int
 }
 #define RSFDE_CH(FN, C, ...)                 \
   do {                                       \
-    if ((C) <= 4) FN<4>(__VA_ARGS__);        \
-    else if ((C) <= 8) FN<8>(__VA_ARGS__);   \
-    else FN<16>(__VA_ARGS__);                \
+    if ((C) <= 2) FN<2>(__VA_ARGS__);        \
+    else if ((C) <= 4) FN<4>(__VA_ARGS__);   \
+    else FN<8>(__VA_ARGS__);                 \
   } while (0)
 
-constexpr int kDcgsChunk = 16;
+// basis vectors per dots / update launch: at most 8 keeps a thread (two elements in flight) within 128
+// registers, two 256-thread blocks per SM; longer bases take several launches (u and w re-read)
+constexpr int kDcgsChunk = 8;
 
 cudaError_t launch_dcgs_dots(const double* const* V, int j, const double* w, double* partial, long long NP, int nblk,
                              const int* skip, cudaStream_t s) {
@@ -781,7 +808,7 @@ cudaError_t launch_dcgs_dots(const double* const* V, int j, const double* w, dou
   const unsigned g = grid_for(NP / 2, nblk);
   const BasisPtrs b = make_basis(V, j + 1);
   const int NT = 2 * j + 2;
-  // chunks of <= 16 basis vectors (u and w are re-read per extra chunk; j < 16 in practice)
+  // chunks of <= kDcgsChunk basis vectors (u and w are re-read per extra chunk)
   for (int i0 = 0; i0 == 0 || i0 < j; i0 += kDcgsChunk) {
     const int cnt = j - i0 < kDcgsChunk ? j - i0 : kDcgsChunk;
     RSFDE_CH(run_dcgs_dots, cnt, g, s, b, i0, cnt, j, i0 == 0 ? 1 : 0, w, partial, NT, NP / 2, skip);
