@@ -155,7 +155,11 @@ rsfde_status rsfde_solve_steps(rsfde_ctx *ctx, int m_begin, int m_count, double 
 
 /* Batched march (the alpha / N sweeps of Tables 1-3, as many
    independent systems at once).  Runs rsfde_solve_steps(ctxs[i], m_begin[i], m_count[i], u[i],
-   F[i], F_static[i], &cfgs[i], &reps[i], streams[i]) for i < count concurrently: one host worker
+   F[i], F_static[i], &cfgs[i], &reps[i], streams[i]) for i < count.  When every system is 1-D and
+   eligible for the on-chip march (see rsfde_solve_steps), all contexts live on one device and no
+   streams are given, the whole batch is ONE kernel launch with one CTA per system (each CTA marches
+   its system with its own n, alpha, restart, tolerance, source and time levels; loop_seconds is then
+   the time of the whole batch; RSFDE_NO_BATCH_KERNEL=1 disables this).  Otherwise: one host worker
    and one CUDA stream per system (streams may be NULL or hold NULL entries: the library then creates
    a non-blocking stream for that system, orders it after the work already queued on the legacy
    default stream, and synchronizes and destroys it before returning; inputs produced on other

@@ -86,6 +86,8 @@ struct OnchipParams {
 };
 size_t onchip_smem_bytes(int n, int restart);
 cudaError_t launch_onchip_1d(const OnchipParams& p, cudaStream_t s);
+// one CTA per system: d_params = device array of count parameter blocks; smem = max over the systems
+cudaError_t launch_onchip_1d_batch(const OnchipParams* d_params, int count, size_t smem, cudaStream_t s);
 
 struct PassParams {
   Geom geo;

@@ -175,7 +175,8 @@ __device__ void on_apply_Pinv(const OnchipCtx& C, const double* in, double* out)
   on_dst(C, t2, out);
 }
 
-__global__ void __launch_bounds__(kOnThreads, 1) onchip_1d_kernel(const OnchipParams P) {
+// the whole CN march of one system by one CTA (the single-system kernel and the batched kernel below)
+__device__ __forceinline__ void onchip_march_body(const OnchipParams& P) {
   extern __shared__ double sm[];
   OnchipCtx C;
   C.P = &P;
@@ -368,6 +369,28 @@ __global__ void __launch_bounds__(kOnThreads, 1) onchip_1d_kernel(const OnchipPa
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) P.X[i] = x[i];
+}
+
+__global__ void __launch_bounds__(kOnThreads, 1) onchip_1d_kernel(const OnchipParams P) { onchip_march_body(P); }
+
+// many independent 1-D systems per launch (the alpha / N sweeps of Tables 1-3,
+// P:528-636), one CTA per system, each with its own parameters, tables, source and solution
+__global__ void __launch_bounds__(kOnThreads, 1) onchip_1d_batch_kernel(const OnchipParams* __restrict__ Ps) {
+  __shared__ OnchipParams sP;
+  if (threadIdx.x == 0) sP = Ps[blockIdx.x];
+  __syncthreads();
+  onchip_march_body(sP);
+}
+
+cudaError_t launch_onchip_1d_batch(const OnchipParams* d_params, int count, size_t smem, cudaStream_t s) {
+  struct Tag {};
+  const int attr = per_device_once<Tag>([](int) -> int {
+    return (int)cudaFuncSetAttribute(onchip_1d_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  });
+  if (attr != (int)cudaSuccess) return attr < 0 ? cudaErrorInvalidDevice : (cudaError_t)attr;
+  if (smem > 220 * 1024 || count < 1) return cudaErrorInvalidValue;
+  onchip_1d_batch_kernel<<<count, kOnThreads, smem, s>>>(d_params);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_onchip_1d(const OnchipParams& p, cudaStream_t s) {

@@ -442,7 +442,7 @@ static rsfde_status dcgs_cycle(rsfde_ctx* c, int form, int m, int restart, int m
   const int nb = reduction_blocks(NP, c->nblk);
   const double vb = 8.0 * (double)NP;
   const int* skip = reinterpret_cast<const int*>(c->d_state);  // converged, breakdown
-  static const bool no_spec = getenv("RSFDE_NO_SPEC") != nullptr;
+  const bool no_spec = getenv("RSFDE_NO_SPEC") != nullptr;  // (read per call: tests toggle it)
   const int lag = (c->profiling || no_spec) ? 0 : 1;
   for (int i = 0; i < 2; ++i)
     if (!c->flag_ev[i]) CK(cudaEventCreateWithFlags(&c->flag_ev[i], cudaEventDisableTiming), "event");
@@ -598,8 +598,9 @@ static bool onchip_eligible(const rsfde_ctx* c, const rsfde_gmres_cfg* cfg) {
   return onchip_smem_bytes(c->n[0], cfg->restart) <= 200 * 1024;
 }
 
-static rsfde_status onchip_march(rsfde_ctx* c, int m_begin, int m_count, const double* F, int F_static, bool f_host,
-                                 const rsfde_gmres_cfg& cfg, cudaStream_t s, rsfde_report* rep, long long* total) {
+// parameters of one on-chip march (tables, F staged to the device when it is host memory)
+static rsfde_status onchip_prepare(rsfde_ctx* c, int m_begin, int m_count, const double* F, int F_static, bool f_host,
+                                   const rsfde_gmres_cfg& cfg, cudaStream_t s, OnchipParams* out) {
   const int n = c->n[0];
   if (!c->d_s0) {
     CK(cudaMalloc(&c->d_s0, n * sizeof(double)), "alloc");
@@ -623,7 +624,7 @@ static rsfde_status onchip_march(rsfde_ctx* c, int m_begin, int m_count, const d
     CK(cudaMemcpyAsync(c->d_on_F, F, nF * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D F");
     Fd = c->d_on_F;
   }
-  OnchipParams p;
+  OnchipParams& p = *out;
   p.n = n;
   p.restart = cfg.restart;
   p.max_iters = cfg.max_iters > 0 ? cfg.max_iters : 10 * cfg.restart;
@@ -647,14 +648,17 @@ static rsfde_status onchip_march(rsfde_ctx* c, int m_begin, int m_count, const d
   p.iters = c->d_on_iters;
   p.relres = c->d_on_relres;
   p.conv = c->d_on_conv;
-  LAUNCH(PC_OPER_SPEC, 0.0, launch_onchip_1d(p, s), "on-chip march");
+  return RSFDE_OK;
+}
+
+// per-step results of an on-chip march into the report (after the stream was synchronised)
+static rsfde_status onchip_collect(rsfde_ctx* c, int m_count, rsfde_report* rep, long long* total) {
   std::vector<int> its(m_count);
   std::vector<double> rr(m_count);
   std::vector<unsigned char> cv(m_count);
-  CK(cudaMemcpyAsync(its.data(), c->d_on_iters, m_count * sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(rr.data(), c->d_on_relres, m_count * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaMemcpyAsync(cv.data(), c->d_on_conv, m_count, cudaMemcpyDeviceToHost, s), "D2H");
-  CK(cudaStreamSynchronize(s), "stream sync");
+  CK(cudaMemcpy(its.data(), c->d_on_iters, m_count * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+  CK(cudaMemcpy(rr.data(), c->d_on_relres, m_count * sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+  CK(cudaMemcpy(cv.data(), c->d_on_conv, m_count, cudaMemcpyDeviceToHost), "D2H");
   *total = 0;
   for (int k = 0; k < m_count; ++k) {
     if (its[k] > 0) *total += its[k];
@@ -665,6 +669,15 @@ static rsfde_status onchip_march(rsfde_ctx* c, int m_begin, int m_count, const d
     }
   }
   return RSFDE_OK;
+}
+
+static rsfde_status onchip_march(rsfde_ctx* c, int m_begin, int m_count, const double* F, int F_static, bool f_host,
+                                 const rsfde_gmres_cfg& cfg, cudaStream_t s, rsfde_report* rep, long long* total) {
+  OnchipParams p;
+  TRY(onchip_prepare(c, m_begin, m_count, F, F_static, f_host, cfg, s, &p));
+  LAUNCH(PC_OPER_SPEC, 0.0, launch_onchip_1d(p, s), "on-chip march");
+  CK(cudaStreamSynchronize(s), "stream sync");
+  return onchip_collect(c, m_count, rep, total);
 }
 
 // ------------------------------------------------------------------------------ ABI
@@ -1063,6 +1076,74 @@ rsfde_status rsfde_solve_steps(rsfde_ctx* c, int m_begin, int m_count, double* u
   return RSFDE_OK;
 }
 
+// NEXT-4 batched kernel: every system of the batch marches in its own CTA of ONE launch (all 1-D,
+// on-chip eligible, one device); u / F may be host or device memory per system
+static rsfde_status onchip_batch(int count, rsfde_ctx* const* ctxs, const int* m_begin, const int* m_count,
+                                 double* const* u, const double* const* F, const int* F_static,
+                                 const rsfde_gmres_cfg* cfgs, rsfde_report* reps) {
+  rsfde_ctx* c = ctxs[0];  // error reporting + LAUNCH accounting of the shared launch
+  CK(cudaSetDevice(c->device), "set device");
+  cudaStream_t s = nullptr;
+  cudaEvent_t ready = nullptr, e0 = nullptr, e1 = nullptr;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+  CK(cudaEventRecord(ready, cudaStreamLegacy), "event");
+  CK(cudaStreamWaitEvent(s, ready, 0), "wait");
+  CK(cudaEventCreate(&e0), "event");
+  CK(cudaEventCreate(&e1), "event");
+  CK(cudaEventRecord(e0, s), "event");
+  std::vector<OnchipParams> ps(count);
+  std::vector<bool> uh(count);
+  size_t smem = 0;
+  for (int i = 0; i < count; ++i) {
+    rsfde_ctx* ci = ctxs[i];
+    uh[i] = is_host_ptr(u[i]);
+    const double* Fi = F ? F[i] : nullptr;
+    const int Fs = F_static ? F_static[i] : 1;
+    {
+      rsfde_ctx* c = ci;  // (the macros report into the system's context)
+      TRY(load_dense(c, u[i], uh[i], c->X, s));
+      TRY(onchip_prepare(c, m_begin[i], m_count[i], Fi, Fs, Fi ? is_host_ptr(Fi) : false, cfgs[i], s, &ps[i]));
+    }
+    const size_t b = onchip_smem_bytes(ci->n[0], cfgs[i].restart);
+    smem = b > smem ? b : smem;
+  }
+  OnchipParams* d_ps = nullptr;
+  CK(cudaMallocAsync((void**)&d_ps, count * sizeof(OnchipParams), s), "alloc params");
+  CK(cudaMemcpyAsync(d_ps, ps.data(), count * sizeof(OnchipParams), cudaMemcpyHostToDevice, s), "params");
+  LAUNCH(PC_OPER_SPEC, 0.0, launch_onchip_1d_batch(d_ps, count, smem, s), "batched on-chip march");
+  for (int i = 0; i < count; ++i) {
+    rsfde_ctx* c = ctxs[i];
+    const long long N = c->n[0];
+    if (uh[i]) {
+      CKL(launch_unpack(c->X, c->Z, c->geo, s), "unpack");
+      CK(cudaMemcpyAsync(u[i], c->Z, N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    } else {
+      CKL(launch_unpack(c->X, u[i], c->geo, s), "unpack");
+    }
+  }
+  CK(cudaEventRecord(e1, s), "event");
+  CK(cudaFreeAsync(d_ps, s), "free params");
+  CK(cudaStreamSynchronize(s), "sync");
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+  for (int i = 0; i < count; ++i) {
+    long long total = 0;
+    rsfde_report* rep = reps ? &reps[i] : nullptr;
+    TRY(onchip_collect(ctxs[i], m_count[i], rep, &total));
+    if (rep) {
+      rep->loop_seconds = ms * 1e-3;  // the whole batch (one launch)
+      rep->setup_seconds = ctxs[i]->setup_seconds;
+      rep->total_iters = total;
+    }
+  }
+  cudaEventDestroy(ready);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(s);
+  return RSFDE_OK;
+}
+
 rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx* const* ctxs, const int* m_begin, const int* m_count,
                                      double* const* u, const double* const* F, const int* F_static,
                                      const rsfde_gmres_cfg* cfgs, rsfde_report* reps, void* const* streams) {
@@ -1073,6 +1154,19 @@ rsfde_status rsfde_solve_steps_batch(int count, rsfde_ctx* const* ctxs, const in
         if (ctxs[i]) ctxs[i]->err = "rsfde_solve_steps_batch: a context appears twice in the batch";
         return RSFDE_E_CONFIG;
       }
+  // all systems 1-D and on-chip eligible on one device (and no caller streams): one launch, one CTA
+  // per system (RSFDE_NO_BATCH_KERNEL=1 selects the stream-per-system path below)
+  {
+    const bool no_kernel = getenv("RSFDE_NO_BATCH_KERNEL") != nullptr;
+    bool all = count >= 1 && !no_kernel;
+    for (int i = 0; all && i < count; ++i) {
+      const rsfde_ctx* c = ctxs[i];
+      all = c && (!streams || !streams[i]) && c->device == ctxs[0]->device && m_begin[i] >= 0 && m_count[i] > 0 &&
+            m_begin[i] + m_count[i] <= c->M && check_cfg(const_cast<rsfde_ctx*>(c), &cfgs[i]) == RSFDE_OK &&
+            onchip_eligible(c, &cfgs[i]);
+    }
+    if (all) return onchip_batch(count, ctxs, m_begin, m_count, u, F, F_static, cfgs, reps);
+  }
   std::vector<rsfde_status> st(count, RSFDE_OK);
   std::vector<cudaStream_t> own(count, nullptr);
   // Streams the library creates are ordered after the work already queued on the legacy default

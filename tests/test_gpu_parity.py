@@ -319,6 +319,49 @@ def test_batched_march_equals_separate_marches():
     for a, b, ra, rb in zip(u_sep, u_bat, rep_sep, rep_bat):
         assert ra["iters"] == rb["iters"] and all(rb["converged"])
         assert torch.equal(a, b)                      # bit-identical: same kernels, deterministic sums
+    for p, ub, rb in zip(probs, u_bat, rep_bat):      # and every system against the oracle
+        _check_march_vs_oracle(p, _host(ub), rb)
+
+
+def _check_march_vs_oracle(p, u, rep, restart=None):
+    Fst = scheme.source_F(p, 0) if p.source_static else None
+    uo, ro, _ = scheme.solve(p, F_static=Fst, restart=restart)
+    assert all(rep["converged"]) and max(abs(a - b) for a, b in zip(rep["iters"], ro.iters)) <= 1, \
+        (p.name, rep["iters"], ro.iters)
+    if rep["iters"] != ro.iters:
+        uo, ro, _ = scheme.solve(p, F_static=Fst, restart=restart, fixed_iters=rep["iters"])
+    assert relerr(u, uo) < 1e-9, (p.name, relerr(u, uo))
+
+
+def test_batched_onchip_kernel_sweep_vs_oracle(monkeypatch):
+    # NEXT-4 as one launch: a Table-1-style alpha x N sweep of 1-D systems (Example 1, P:523-526,
+    # alpha in {1.3, 1.5, 1.9}, N+1 in {16, 32, 64}) plus a C1-shaped system, one CTA per system;
+    # every system is checked against the oracle and against its own separate march
+    from paper_2404_10221_b200 import solver as SV
+    probs = [I.example(1, n1 - 1, 32, (a,)) for a in (1.3, 1.5, 1.9) for n1 in (16, 32, 64)]
+    probs.append(I.config_c1(n=255, M=16))
+    sols = [_solver(p) for p in probs]
+    Fs = [torch.stack([S.compact_source(_dev(p.f_closed(p.t_half(m)))) for m in range(p.M)])
+          for S, p in zip(sols, probs)]
+    cfgs = [S.cfg(restart=p.restart, tol=p.tol) for S, p in zip(sols, probs)]
+    u_bat = [_dev(p.psi_interior()) for p in probs]
+    n0 = [S.launch_count(reset=True) for S in sols]
+    rep_bat = SV.solve_steps_batch(sols, u_bat, Fs=Fs, F_static=[False] * len(probs), cfgs=cfgs)
+    # one batched launch accounted on the first context, nothing but pack/unpack on the others
+    assert sols[0].launch_count() <= 2 * len(probs) + 1
+    for p, ub, rb in zip(probs, u_bat, rep_bat):
+        _check_march_vs_oracle(p, _host(ub), rb)
+    # the same systems one by one (single-system on-chip kernel): identical results
+    for S, p, F, c, ub, rb in zip(sols, probs, Fs, cfgs, u_bat, rep_bat):
+        u1 = _dev(p.psi_interior())
+        r1 = S.solve_steps(u1, F=F, F_static=False, cfg=c)
+        assert r1["iters"] == rb["iters"] and torch.equal(u1, ub)
+    # and the stream-per-system path agrees
+    monkeypatch.setenv("RSFDE_NO_BATCH_KERNEL", "1")
+    u_thr = [_dev(p.psi_interior()) for p in probs]
+    rep_thr = SV.solve_steps_batch(sols, u_thr, Fs=Fs, F_static=[False] * len(probs), cfgs=cfgs)
+    for a, b, ra, rb in zip(u_thr, u_bat, rep_thr, rep_bat):
+        assert ra["iters"] == rb["iters"] and torch.equal(a, b)
 
 
 def test_batched_march_rejects_duplicate_contexts():
