@@ -221,6 +221,12 @@ rsfde_status rsfde_nccl_unique_id(void *out128);
 rsfde_status rsfde_team_setup(rsfde_team **out, const rsfde_problem *p, int nranks, int rank, int nlocal,
                               const void *nccl_id, void *stream);
 rsfde_status rsfde_team_slab(const rsfde_team *t, int local, int *x1_lo, int *x1_count);
+/* Host-only slab bookkeeping (no device needed): for rank of nranks on the grid n[3], out[0..5] =
+   {x1_lo, x1_count (layout A slab; the last rank's count excludes the x1 pad plane), x2_lo, x2_count
+   (layout T slab), s = (n1+1)/nranks, s2 = (n2+1)/nranks}; *block_elems = s2*n3*s, the doubles a rank
+   sends to each peer per transposed vector, laid out [x2 local < s2][x3 < n3][x1 local < s].
+   RSFDE_E_DIM unless nranks divides n1+1 and n2+1; RSFDE_E_CONFIG for bad rank / nranks (1..8). */
+rsfde_status rsfde_team_partition(const int n[3], int nranks, int rank, int out[6], long long *block_elems);
 /* op: RSFDE_OP_K (P_hat^{-1} A) or RSFDE_OP_A */
 rsfde_status rsfde_team_matvec(rsfde_team *t, int op, int m, const double *x, double *y, void *stream);
 rsfde_status rsfde_team_precond_apply(rsfde_team *t, int kind, const double *x, double *y, void *stream);

@@ -559,6 +559,37 @@ static rsfde_status team_gmres(rsfde_team* t, int m, bool fast, bool have_b, con
       std::vector<double*> zs(nl);
       for (int l = 0; l < nl; ++l) zs[l] = t->sh[l].Z;
       TTRY(team_chain(t, a, zs.data(), s));
+      if (t->tab->ortho == ORTHO_DCGS2) {
+        // DCGS2 (krylov_kernels.cu): local dots -> one allreduce of the 2j+2 sums -> re-orthogonalise /
+        // Hessenberg on every rank; local update -> one allreduce of ||u'||^2 -> rotation, flags.
+        // Two allreduces per Arnoldi step (CGS2: three).
+        const int NT = 2 * j + 2;
+        for (int l = 0; l < nl; ++l) {
+          ShardBufs& b = t->sh[l];
+          const double* const* Vp = (const double* const*)b.V.data();
+          TCKL(launch_dcgs_dots(Vp, j, b.Z, b.part, NP, t->tab->nblk, nullptr, s), "dcgs dots");
+          TCKL(launch_reduce(b.part, nb, NT, b.h1, s), "reduce dots");
+        }
+        TTRY(team_allreduce(t, [&](int l) { return t->sh[l].h1; }, NT, s));
+        for (int l = 0; l < nl; ++l) {
+          ShardBufs& b = t->sh[l];
+          const double* const* Vp = (const double* const*)b.V.data();
+          TCKL(launch_dcgs_finish_a(b.st, b.h1, 1, j, b.vscale, nullptr, s), "dcgs finish a");
+          TCKL(launch_dcgs_update(Vp, j, b.st, b.Z, b.nrm, NP, t->tab->nblk, nullptr, s), "dcgs update");
+          TCKL(launch_reduce(b.nrm, nb, 1, b.red, s), "reduce nrm");
+        }
+        TTRY(team_allreduce(t, [&](int l) { return t->sh[l].red; }, 1, s));
+        for (int l = 0; l < nl; ++l) {
+          ShardBufs& b = t->sh[l];
+          TCKL(launch_dcgs_finish_b(b.st, b.red, 1, j, tol, b.vscale, nullptr, s), "dcgs finish b");
+        }
+        ++total;
+        k = j + 1;
+        TTRY(team_flags(t, &fl, s));
+        const bool stop = fixed > 0 ? total >= fixed : fl.converged != 0;
+        if (stop || fl.breakdown || total >= max_iters) break;
+        continue;
+      }
       for (int l = 0; l < nl; ++l) {
         ShardBufs& b = t->sh[l];
         const double* const* Vp = (const double* const*)b.V.data();
@@ -706,9 +737,12 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
   for (int l = 0; l < nlocal; ++l) {
     ShardBufs& b = t->sh[l];
     const int r = rank + l;
-    b.x1lo = r * t->s;
-    b.x2lo = r * t->s2;
-    b.s_real = std::max(0, std::min(t->s, n1 - b.x1lo));
+    int part[6];
+    long long blk = 0;
+    if ((st = rsfde_team_partition(p->n, nranks, r, part, &blk)) != RSFDE_OK || blk != t->blk) return fail(RSFDE_E_DIM);
+    b.x1lo = part[0];
+    b.x2lo = part[2];
+    b.s_real = part[1];
     b.gA.d = 3;
     b.gA.n[0] = t->s;
     b.gA.n[1] = n2;
@@ -730,8 +764,8 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     if ((st = talloc(t, &b.recv, (size_t)(nranks * t->blk))) != RSFDE_OK) return fail(st);
     double** sm[] = {&b.vscale, &b.h1, &b.h2, &b.red};
     for (double** v : sm)
-      if ((st = talloc(t, v, 64)) != RSFDE_OK) return fail(st);
-    if ((st = talloc(t, &b.part, (size_t)t->tab->nblk * 64)) != RSFDE_OK) return fail(st);
+      if ((st = talloc(t, v, 128)) != RSFDE_OK) return fail(st);  // (DCGS2: 2j+2 <= 100 sums)
+    if ((st = talloc(t, &b.part, (size_t)t->tab->nblk * 128)) != RSFDE_OK) return fail(st);
     if ((st = talloc(t, &b.nrm, (size_t)t->tab->nblk)) != RSFDE_OK) return fail(st);
     double* stp = nullptr;
     if ((st = talloc(t, &stp, (sizeof(GmresState) + 7) / 8)) != RSFDE_OK) return fail(st);
@@ -749,6 +783,21 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     if (r != ncclSuccess) return fail(nfail(t, r, "ncclCommInitRank"));
   }
   *out = t;
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_team_partition(const int n[3], int nranks, int rank, int out[6], long long* block_elems) {
+  if (!n || !out || nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks) return RSFDE_E_CONFIG;
+  if (n[0] < 1 || n[1] < 1 || n[2] < 1) return RSFDE_E_DIM;
+  if ((n[0] + 1) % nranks || (n[1] + 1) % nranks) return RSFDE_E_DIM;
+  const int s = (n[0] + 1) / nranks, s2 = (n[1] + 1) / nranks;
+  out[0] = rank * s;                                     // x1 slab (layout A)
+  out[1] = std::max(0, std::min(s, n[0] - out[0]));      // (the last rank holds the x1 pad plane)
+  out[2] = rank * s2;                                    // x2 slab (layout T)
+  out[3] = std::max(0, std::min(s2, n[1] - out[2]));
+  out[4] = s;
+  out[5] = s2;
+  if (block_elems) *block_elems = (long long)s2 * n[2] * s;  // all-to-all block [x2l < s2][x3 < n3][x1l < s]
   return RSFDE_OK;
 }
 

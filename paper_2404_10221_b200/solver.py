@@ -285,6 +285,20 @@ def solve_steps_batch(solvers, us, Fs=None, F_static=None, m_begin=None, m_count
     return out
 
 
+def team_partition(n, nranks: int, rank: int):
+    """rsfde_team_partition (host only, no device needed): the rank's x1 slab (layout A), x2 slab
+    (layout T), the planes per rank s, s2 and the all-to-all block size in doubles."""
+    lib = L.load()
+    nn = (C.c_int * 3)(*[int(v) for v in n])
+    out = (C.c_int * 6)()
+    blk = C.c_longlong()
+    st = lib.rsfde_team_partition(nn, nranks, rank, out, C.byref(blk))
+    if st != L.OK:
+        raise L.RsfdeError(st, "rsfde_team_partition")
+    return {"x1_lo": out[0], "x1_count": out[1], "x2_lo": out[2], "x2_count": out[3], "s": out[4], "s2": out[5],
+            "block": blk.value}
+
+
 class RsfdeTeam:
     """Slab-sharded 3D solver (x_1 slabs over ``nranks`` ranks).
 
