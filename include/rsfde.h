@@ -193,6 +193,13 @@ long long rsfde_device_bytes(const rsfde_ctx *ctx);
 /* Kernel launches issued since setup (or the last reset) -- evidence for bench.py. */
 long long rsfde_launch_count(const rsfde_ctx *ctx, int reset);
 
+/* Replays of the graph-captured first GMRES cycle since setup.  By default (A form, first-cycle
+   residual shortcut, DCGS2) the first cycle of every CN step of rsfde_solve_steps runs as ONE CUDA
+   graph whose Arnoldi steps are conditional nodes gated on the device-side convergence flag (stopping
+   rule P:513), so the host reads the flags once per cycle; RSFDE_NO_GRAPH=1 in the environment selects
+   the stream path (one flags read per Arnoldi step).  Results are bit-identical either way. */
+long long rsfde_graph_replays(const rsfde_ctx *ctx);
+
 /* Optional per-kernel timing: with enable != 0 every kernel launch is bracketed by CUDA events
    on its stream and attributed to one of the classes returned by rsfde_profile_read (0 ..
    count-1: spectral operator passes, physical operator passes, DST passes, CGS2 dots, CGS2

@@ -63,6 +63,7 @@ SIGNATURES = {
     "rsfde_table": (C.c_int, [C.c_void_p, C.c_int, C.c_int, DP]),
     "rsfde_device_bytes": (C.c_longlong, [C.c_void_p]),
     "rsfde_launch_count": (C.c_longlong, [C.c_void_p, C.c_int]),
+    "rsfde_graph_replays": (C.c_longlong, [C.c_void_p]),
     "rsfde_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "rsfde_profile_read": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_longlong), DP, DP,
                                      C.POINTER(C.c_char_p)]),

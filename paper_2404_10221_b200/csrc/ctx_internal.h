@@ -20,6 +20,21 @@ struct rsfde_ctx {
   int nblk = 0;    // blocks (= partial sums) of the streaming reductions: 8 per SM of that device
   int ortho = 0;   // ORTHO_DCGS2 | ORTHO_CGS2
   const int* skip = nullptr;             // device flags of the speculative Arnoldi launches (PassParams::skip)
+  // graph-captured first GMRES cycle of a CN step (rsfde_host.cu gmres_graph): r0, the Arnoldi steps as
+  // nested conditional IF nodes and the y solve / x update as a SWITCH on the column count.  The time
+  // level reaches the captured kernels through the device slot d_ab = {a(t), b(t)} (ECoef::ab).
+  struct StepGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int restart = 0, max_iters = 0, fixed = 0, nsteps = 0;
+    double tol = 0;
+    long long launches_pre = 0;
+    std::vector<long long> launches_step, launches_end;  // per Arnoldi step j / per final column count k
+  } sg;
+  long long graph_replays = 0;
+  double* d_ab = nullptr;
+  bool ab_dev = false;  // rsfde_ecoef_at points ECoef::ab at d_ab (set while capturing)
+  cudaStream_t cap_s[2] = {nullptr, nullptr};
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};  // flags copies of the last two Arnoldi steps
   // on-chip 1-D march (lazily allocated): generator table, per-step outputs, device copy of host F
   double* d_s0 = nullptr;

@@ -114,16 +114,13 @@ __device__ __forceinline__ void idft(double2* a) {
 template <int E, bool INV>
 __device__ __forceinline__ void twiddle_col(double2 (&v)[E], const double2* __restrict__ tw, int g, int L) {
   const double2 w1 = __ldg(tw + g);
+  double2 w = w1;
+  // (one flat loop: the nested group loop with a `break` made nvcc keep v[] in local memory for E = 16)
 #pragma unroll
-  for (int a = 0; a < (E + 7) / 8; ++a) {
-    double2 w = (a == 0) ? w1 : __ldg(tw + ((8 * a * g) & (L - 1)));
-#pragma unroll
-    for (int b = (a == 0 ? 1 : 0); b < 8; ++b) {
-      const int k1 = 8 * a + b;
-      if (k1 >= E) break;
-      v[k1] = INV ? c_mulc(v[k1], w) : c_mul(v[k1], w);
-      if (b < 7) w = c_mul(w, w1);
-    }
+  for (int k1 = 1; k1 < E; ++k1) {
+    if ((k1 & 7) == 0) w = __ldg(tw + ((k1 * g) & (L - 1)));
+    else if (k1 > 1) w = c_mul(w, w1);
+    v[k1] = INV ? c_mulc(v[k1], w) : c_mul(v[k1], w);
   }
 }
 

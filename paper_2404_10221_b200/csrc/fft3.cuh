@@ -1,23 +1,27 @@
-// Three-stage FP64 FFT for long pencils, L = 32 * 32 * F (F = 2, 4: L = 2048, 4096 -> n = 1023,
-// 2047; BASELINE config C3).  One pencil pair per CTA of G = 32 F threads, E = 32 complex values
-// per thread, two XOR-swizzled shared-memory exchanges, __syncthreads as the group barrier.
+// Three-stage FP64 FFT L = E * E * F held by G = E F threads (one pencil pair per CTA), E complex
+// values per thread, two XOR-swizzled shared-memory exchanges, __syncthreads as the group barrier.
+// Instances: E = 32, F = 2 / 4 (L = 2048 / 4096, the long pencils of BASELINE C3: throughput form),
+// E = 16, F = 8 / 16 (L = 2048 / 4096 with 2-4x the threads per pair and half the registers: lower
+// latency per pair) and E = 8, F = 8 (L = 512: the latency form for small grids such as C2, where a
+// pass has fewer pencil pairs than the GPU has warps).  Requires F <= E, E % F == 0.
 //
-// Forward, natural input x_j (column layout: thread t holds x[t + G m], m < 32):
+// Forward, natural input x_j (column layout: thread t holds x[t + G m], m < E):
 //   j = t + G m,  t = a + F b,  k = k1 + E c + E^2 e
 //   X_k = sum_{a} W_F^{a e} W_G^{a c} sum_{b} W_E^{b c} [ W_L^{t k1} sum_m W_E^{m k1} x_{t+Gm} ]
-//   stage A: DFT-32 over m, twiddle W_L^{t k1}        (thread t)
-//   stage B: DFT-32 over b, twiddle W_G^{a c}         (thread (k1, a) = (t/F, t%F))
-//   stage C: DFT-F over a                              (thread (k1, a0): c = a0 (32/F) + s)
-// Row layout: register r = s F + e holds X[k1 + E (a0 (32/F) + s) + E^2 e].
+//   stage A: DFT-E over m, twiddle W_L^{t k1}         (thread t)
+//   stage B: DFT-E over b, twiddle W_G^{a c}          (thread (k1, a) = (t/F, t%F))
+//   stage C: DFT-F over a                              (thread (k1, a0): c = a0 (E/F) + s)
+// Row layout: register r = s F + e holds X[k1 + E (a0 (E/F) + s) + E^2 e].
 // The inverse (row -> column) runs the transposed pipeline on conjugated data.
 #pragma once
 #include "fft.cuh"
 
 namespace rsfde {
 
-template <int F>
+template <int E_, int F>
 struct Fft3 {
-  static constexpr int E = 32, G = 32 * F, L = E * G, N = L / 2, CS = E / F;
+  static constexpr int E = E_, G = E * F, L = E * G, N = L / 2, CS = E / F;
+  static_assert(F <= E && E % F == 0, "Fft3: F <= E, F | E");
   static constexpr int SWA = (8 / F > 1) ? (8 / F - 1) : 0;
   __device__ static __forceinline__ int ia(int k1, int tt) { return k1 * G + (tt ^ (F * (k1 & SWA))); }
   __device__ static __forceinline__ int ib(int k1, int a, int c) {

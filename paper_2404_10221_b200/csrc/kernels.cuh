@@ -48,7 +48,12 @@ struct ECoef {
   const double* g[3];        // device, length n_i, or null (= 1)
   const double* k[3];        // device, length n_i, or null (= 0)
   const double* grid;        // kind 2: dense layout [x1][x2][x3], N values
+  const double* ab;          // device {a, b} overriding a, b when non-null (graph-captured steps: the
+                             // time level is written there before each replay)
 };
+__device__ __forceinline__ double2 e_ab(const ECoef& e) {
+  return e.ab ? make_double2(__ldg(e.ab), __ldg(e.ab + 1)) : make_double2(e.a, e.b);
+}
 
 // the last-axis pass divides by Lambda(k):
 //   PHAT: Lambda_P Lambda_H      PALPHA: Lambda_P        PALPHA_SQRT: Lambda_P^{1/2}
@@ -169,6 +174,13 @@ cudaError_t launch_compact_source(const double* f_closed, double* F, const Geom&
 cudaError_t launch_emaxmin(const ECoef& e, const double* a_half, const double* b_half, int M, int grid_static,
                            const Geom& geo, double* partial, int nblk, cudaStream_t s);
 
+// conditional handle of a graph-captured GMRES cycle (rsfde_host.cu graph_build): h_cont gates the next
+// Arnoldi step (its IF node); the kernel that sets it lives in the graph that owns the handle
+struct GraphCond {
+  unsigned long long h_cont = 0;
+  int on = 0;
+};
+
 // GMRES control state on the device (one solve)
 struct GmresState {
   // small fields first: the host reads back the first 24 bytes after every iteration
@@ -189,6 +201,7 @@ struct GmresState {
   double cq[52], cu[52];
   double nu;
   int kcols;            // columns usable by the y solve (j+1, or j after a breakdown in the correction)
+  int steps;            // graph-captured cycle: Arnoldi steps executed (set by gmres_init / dcgs_finish_b)
 };
 // number of blocks (= partial sums) every streaming reduction uses for a vector of length NP
 int reduction_blocks(long long NP, int nblk);
@@ -198,7 +211,7 @@ cudaError_t launch_arnoldi_finish(GmresState* st, const double* h1, const double
                                   double* vscale_next, cudaStream_t s);
 // beta = ||r0||: st->g = [beta,0..], beta0, vscale[0] = 1/beta
 cudaError_t launch_gmres_init(GmresState* st, const double* partial_nrm, int nblk, double* vscale0,
-                              int first_cycle, cudaStream_t s);
+                              int first_cycle, cudaStream_t s, GraphCond gc = GraphCond());
 // y = R^{-1} g for k columns
 cudaError_t launch_gmres_solve_y(GmresState* st, int k, cudaStream_t s);
 
@@ -216,6 +229,10 @@ cudaError_t launch_dcgs_update(const double* const* V, int j, const GmresState* 
                                double* partial_nrm, long long NP, int nblk, const int* skip, cudaStream_t s);
 // tentative subdiagonal h_{j+1,j}, rotation of column j, convergence flag, vscale[j+1]
 cudaError_t launch_dcgs_finish_b(GmresState* st, const double* partial_nrm, int nblk, int j, double tol,
-                                 double* vscale, const int* skip, cudaStream_t s);
+                                 double* vscale, const int* skip, cudaStream_t s, GraphCond gc = GraphCond());
+// SWITCH handle <- st->kcols (the y solve / x update variant of a captured cycle)
+cudaError_t launch_graph_set_k(const GmresState* st, unsigned long long hk, cudaStream_t s);
+// device {a, b} slot of a graph-captured step (ECoef::ab)
+cudaError_t launch_set_ab(double* ab, double a, double b, cudaStream_t s);
 
 }  // namespace rsfde

@@ -249,9 +249,13 @@ __global__ void __launch_bounds__(256) arnoldi_finish_kernel(GmresState* st, con
 }
 
 __global__ void gmres_init_kernel(GmresState* st, const double* __restrict__ pnrm, int nblk, double* vscale0,
-                                  int first_cycle) {
+                                  int first_cycle, GraphCond gc) {
   const double nrm2 = block_sum_partials(pnrm, nblk);
   if (threadIdx.x != 0) return;
+  if (gc.on) {  // graph-captured cycle: Arnoldi steps run while r0 != 0; no column yet
+    st->steps = 0;
+    cudaGraphSetConditional(gc.h_cont, nrm2 > 0.0 ? 1u : 0u);
+  }
   const double beta = sqrt(nrm2);
   for (int i = 0; i < kLdH; ++i) st->g[i] = 0.0;
   st->g[0] = beta;
@@ -526,8 +530,16 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
 }
 
 __global__ void __launch_bounds__(256) dcgs_finish_b_kernel(GmresState* st, const double* __restrict__ pnrm, int nblk,
-                                                            int j, double tol, double* vscale, const int* skip) {
-  if (skip_launch(skip)) return;  // (uniform over the block, before the reduction's barriers)
+                                                            int j, double tol, double* vscale, const int* skip,
+                                                            GraphCond gc) {
+  if (skip_launch(skip)) {  // (uniform over the block, before the reduction's barriers)
+    // lucky breakdown in finish_a: stop the captured cycle with finish_a's column count
+    if (gc.on && threadIdx.x == 0) {
+      st->steps = j + 1;
+      if (gc.h_cont) cudaGraphSetConditional(gc.h_cont, 0u);
+    }
+    return;
+  }
   const double nrm2 = block_sum_partials(pnrm, nblk);
   if (threadIdx.x != 0) return;
   double* Hr = st->Hraw;
@@ -543,6 +555,10 @@ __global__ void __launch_bounds__(256) dcgs_finish_b_kernel(GmresState* st, cons
   st->converged = st->relres <= tol ? 1 : 0;
   st->breakdown = (un == 0.0) ? 1 : 0;
   st->kcols = j + 1;
+  if (gc.on) {
+    st->steps = j + 1;
+    if (gc.h_cont) cudaGraphSetConditional(gc.h_cont, (st->converged | st->breakdown) ? 0u : 1u);
+  }
 }
 
 // dense [rows][n_d] <-> padded [rows][P]
@@ -775,8 +791,8 @@ cudaError_t launch_arnoldi_finish(GmresState* st, const double* h1, const double
 }
 
 cudaError_t launch_gmres_init(GmresState* st, const double* partial_nrm, int nblk, double* vscale0, int first_cycle,
-                              cudaStream_t s) {
-  gmres_init_kernel<<<1, 256, 0, s>>>(st, partial_nrm, nblk, vscale0, first_cycle);
+                              cudaStream_t s, GraphCond gc) {
+  gmres_init_kernel<<<1, 256, 0, s>>>(st, partial_nrm, nblk, vscale0, first_cycle, gc);
   return cudaGetLastError();
 }
 
@@ -838,13 +854,31 @@ cudaError_t launch_dcgs_update(const double* const* V, int j, const GmresState* 
 }
 
 cudaError_t launch_dcgs_finish_b(GmresState* st, const double* partial_nrm, int nblk, int j, double tol, double* vscale,
-                                 const int* skip, cudaStream_t s) {
-  dcgs_finish_b_kernel<<<1, 256, 0, s>>>(st, partial_nrm, nblk, j, tol, vscale, skip);
+                                 const int* skip, cudaStream_t s, GraphCond gc) {
+  dcgs_finish_b_kernel<<<1, 256, 0, s>>>(st, partial_nrm, nblk, j, tol, vscale, skip, gc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_gmres_solve_y(GmresState* st, int k, cudaStream_t s) {
   gmres_solve_y_kernel<<<1, 32, 0, s>>>(st, k);
+  return cudaGetLastError();
+}
+
+// SWITCH selector of a captured cycle: the column count of the y solve (kcols < 0: r0 == 0, none)
+__global__ void graph_set_k_kernel(const GmresState* st, unsigned long long hk) {
+  cudaGraphSetConditional(hk, st->kcols > 0 ? (unsigned)st->kcols : 0u);
+}
+cudaError_t launch_graph_set_k(const GmresState* st, unsigned long long hk, cudaStream_t s) {
+  graph_set_k_kernel<<<1, 1, 0, s>>>(st, hk);
+  return cudaGetLastError();
+}
+
+__global__ void set_ab_kernel(double* ab, double a, double b) {
+  ab[0] = a;
+  ab[1] = b;
+}
+cudaError_t launch_set_ab(double* ab, double a, double b, cudaStream_t s) {
+  set_ab_kernel<<<1, 1, 0, s>>>(ab, a, b);
   return cudaGetLastError();
 }
 

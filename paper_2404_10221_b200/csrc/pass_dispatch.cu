@@ -7,6 +7,10 @@ cudaError_t launch_oper_1024(const PassParams& p, bool spectral, bool last, cuda
 cudaError_t launch_dst_1024(const PassParams& p, bool last, cudaStream_t s);
 cudaError_t launch_oper_512(const PassParams& p, bool spectral, bool last, cudaStream_t s);
 cudaError_t launch_dst_512(const PassParams& p, bool last, cudaStream_t s);
+cudaError_t launch_oper_2048(const PassParams& p, bool spectral, bool last, cudaStream_t s);
+cudaError_t launch_dst_2048(const PassParams& p, bool last, cudaStream_t s);
+cudaError_t launch_oper_4096(const PassParams& p, bool spectral, bool last, cudaStream_t s);
+cudaError_t launch_dst_4096(const PassParams& p, bool last, cudaStream_t s);
 extern template cudaError_t launch_oper_t<Lay2<2, 2>>(const PassParams&, bool, bool, cudaStream_t);
 extern template cudaError_t launch_dst_t<Lay2<2, 2>>(const PassParams&, bool, cudaStream_t);
 extern template cudaError_t launch_oper_t<Lay2<4, 2>>(const PassParams&, bool, bool, cudaStream_t);
@@ -25,10 +29,6 @@ extern template cudaError_t launch_oper_t<Lay2<32, 16>>(const PassParams&, bool,
 extern template cudaError_t launch_dst_t<Lay2<32, 16>>(const PassParams&, bool, cudaStream_t);
 extern template cudaError_t launch_oper_t<Lay2<32, 32>>(const PassParams&, bool, bool, cudaStream_t);
 extern template cudaError_t launch_dst_t<Lay2<32, 32>>(const PassParams&, bool, cudaStream_t);
-extern template cudaError_t launch_oper_t<Lay3<2>>(const PassParams&, bool, bool, cudaStream_t);
-extern template cudaError_t launch_dst_t<Lay3<2>>(const PassParams&, bool, cudaStream_t);
-extern template cudaError_t launch_oper_t<Lay3<4>>(const PassParams&, bool, bool, cudaStream_t);
-extern template cudaError_t launch_dst_t<Lay3<4>>(const PassParams&, bool, cudaStream_t);
 
 cudaError_t launch_oper_pass(const PassParams& p, bool spectral, bool last, cudaStream_t s) {
   switch (p.L) {
@@ -41,8 +41,8 @@ cudaError_t launch_oper_pass(const PassParams& p, bool spectral, bool last, cuda
     case 256: return launch_oper_t<Lay2<32, 8>>(p, spectral, last, s);
     case 512: return launch_oper_512(p, spectral, last, s);
     case 1024: return launch_oper_1024(p, spectral, last, s);
-    case 2048: return launch_oper_t<Lay3<2>>(p, spectral, last, s);
-    case 4096: return launch_oper_t<Lay3<4>>(p, spectral, last, s);
+    case 2048: return launch_oper_2048(p, spectral, last, s);
+    case 4096: return launch_oper_4096(p, spectral, last, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -58,8 +58,8 @@ cudaError_t launch_dst_pass(const PassParams& p, bool last, cudaStream_t s) {
     case 256: return launch_dst_t<Lay2<32, 8>>(p, last, s);
     case 512: return launch_dst_512(p, last, s);
     case 1024: return launch_dst_1024(p, last, s);
-    case 2048: return launch_dst_t<Lay3<2>>(p, last, s);
-    case 4096: return launch_dst_t<Lay3<4>>(p, last, s);
+    case 2048: return launch_dst_2048(p, last, s);
+    case 4096: return launch_dst_4096(p, last, s);
     default: return cudaErrorInvalidValue;
   }
 }

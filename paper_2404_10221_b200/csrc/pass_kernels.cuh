@@ -186,7 +186,8 @@ __device__ __forceinline__ void st_pair(const PassParams& p, double* X, const Pa
 }
 
 // e(x, t) of both pencils at axis position j (1..n)
-__device__ __forceinline__ double2 e_pair(const PassParams& p, const PairCtx& pc, const PencilConsts& kc, int j) {
+__device__ __forceinline__ double2 e_pair(const PassParams& p, const PairCtx& pc, const PencilConsts& kc, int j,
+                                          double2 eab) {
   const ECoef& E = p.e;
   if (E.kind == 2) {
     // dense stride of the axis (d <= 3: at most two later axes)
@@ -197,7 +198,7 @@ __device__ __forceinline__ double2 e_pair(const PassParams& p, const PairCtx& pc
   }
   const double ga = E.g[p.axis] ? __ldg(E.g[p.axis] + j - 1) : 1.0;
   const double ka = E.k[p.axis] ? __ldg(E.k[p.axis] + j - 1) : 0.0;
-  return make_double2(fma(E.b * kc.eP_p, ga, E.a) + (kc.eK_p + ka), fma(E.b * kc.eP_q, ga, E.a) + (kc.eK_q + ka));
+  return make_double2(fma(eab.y * kc.eP_p, ga, eab.x) + (kc.eK_p + ka), fma(eab.y * kc.eP_q, ga, eab.x) + (kc.eK_q + ka));
 }
 
 // Lambda of both pencils at last-axis spectral index k (1..n)
@@ -306,12 +307,13 @@ struct Lay2 {
     fft_any<E, G>(v, buf, g, tw, inv);
   }
 };
-// Lay3: three-stage FFT (fft3.cuh), one pair per CTA of 32 F threads, CTA-level sync.
-template <int F>
+// Lay3: three-stage FFT (fft3.cuh), one pair per CTA of E F threads, CTA-level sync.
+template <int E_, int F>
 struct Lay3 {
-  using FT = Fft3<F>;
+  using FT = Fft3<E_, F>;
   static constexpr int E = FT::E, G = FT::G, L = FT::L, N = FT::N, GROUPS = 1, THREADS = FT::G;
-  static constexpr int MINB = F == 2 ? 6 : 3;
+  // E = 32: 3 / 6 CTAs per SM (L = 4096 / 2048, as measured in round 1); E <= 16: 128 registers
+  static constexpr int MINB = E == 32 ? (F == 2 ? 6 : 3) : (65536 / 128) / THREADS;
   __device__ static __forceinline__ void sync() { __syncthreads(); }
   __device__ static __forceinline__ int rowk(int t, int r) { return FT::rowk(t, r); }
   __host__ __device__ static constexpr bool lower(int r) { return FT::lower(r); }
@@ -381,8 +383,9 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
     }
 
     // phases: OPER: 0 conv-fwd, 1 conv-inv, 2 dst(y) [, 3 second dst]; DST: 2 dst [, 3 second dst]
-    const int first = OPER ? 0 : 2;
-    const int last_phase = OPER && !SPECTRAL ? 1 : (LAST ? 3 : 2);
+    constexpr int first = OPER ? 0 : 2;
+    constexpr int last_phase = OPER && !SPECTRAL ? 1 : (LAST ? 3 : 2);
+    // one rolled phase loop: one copy of each FFT body (smaller code, fewer live registers)
 #pragma unroll 1
     for (int ph = first; ph <= last_phase; ++ph) {
       T::fft(v, buf, g, p.tw, ph == 1);
@@ -410,6 +413,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
         // conv inverse done: column layout, T R at j = g + G m (m < E/2).
         // X channel at j, neighbours through the shared buffer
         const PencilConsts kc = (p.xmode == X_E_TIMES_R) ? make_consts(p, pc) : PencilConsts{};
+        const double2 eab = e_ab(p.e);
         T::sync();
 #pragma unroll
         for (int m = 0; m < E / 2; ++m) {
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
               x = ld_pair(p, p.X, pc, j);
             } else if (p.xmode == X_E_TIMES_R) {
               const double2 r = ld_pair(p, p.R, pc, j);
-              const double2 e = e_pair(p, pc, kc, j);
+              const double2 e = e_pair(p, pc, kc, j, eab);
               x = make_double2(rs * r.x * e.x, rs * r.y * e.y);
             }
           }

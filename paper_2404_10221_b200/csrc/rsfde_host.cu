@@ -229,6 +229,7 @@ PassParams rsfde_axis_params(const rsfde_ctx* c, int axis) {
 ECoef rsfde_ecoef_at(const rsfde_ctx* c, int m) {
   ECoef e;
   memset(&e, 0, sizeof e);
+  if (c->ab_dev) e.ab = c->d_ab;
   if (c->ekind == RSFDE_COEF_GRID) {
     e.kind = 2;
     e.grid = c->grid + (c->grid_static ? 0 : (long long)m * c->n[0] * c->n[1] * c->n[2]);
@@ -486,6 +487,221 @@ static rsfde_status dcgs_cycle(rsfde_ctx* c, int form, int m, int restart, int m
   return RSFDE_OK;
 }
 
+// ------------------------------------------------------------------------------ graph-captured cycle
+// The first GMRES cycle of a CN step (A form, first-cycle residual shortcut) as ONE CUDA graph: the r0
+// chain, ||r0||, then Arnoldi step j as the body of a conditional IF node nested in step j-1's body (the
+// node's handle is cleared on the device by dcgs_finish_b on convergence or breakdown, so nothing after
+// the last step is launched or evaluated), then a SWITCH on the final column count k running the y
+// solve and x += V y for that k.  The host reads the flags once per cycle instead of once per Arnoldi
+// step (stopping rule P:513).  RSFDE_NO_GRAPH=1 selects the stream path.  (A handle
+// gates exactly one conditional node and is set from the graph that owns it, hence one handle per body.)
+static bool graph_eligible(const rsfde_ctx* c, int form, bool mode_fast) {
+  if (c->profiling || getenv("RSFDE_NO_GRAPH")) return false;  // (read per call: tests toggle it)
+  if (c->ortho != ORTHO_DCGS2 || form != RSFDE_FORM_A || !mode_fast) return false;
+  return c->ekind != RSFDE_COEF_GRID || c->grid_static;
+}
+
+static void graph_destroy(rsfde_ctx* c) {
+  for (cudaStream_t cs : c->cap_s) {  // (a capture abandoned by an error)
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cs && cudaStreamIsCapturing(cs, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+      cudaGraph_t junk = nullptr;
+      if (cudaStreamEndCapture(cs, &junk) == cudaSuccess && junk) cudaGraphDestroy(junk);
+    }
+  }
+  cudaGetLastError();
+  if (c->sg.exec) cudaGraphExecDestroy(c->sg.exec);
+  if (c->sg.graph) cudaGraphDestroy(c->sg.graph);
+  c->sg = rsfde_ctx::StepGraph();
+}
+
+// conditional node after the capture frontier of cs; it becomes the new frontier
+static cudaError_t add_cond(cudaStream_t cs, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                            unsigned size, cudaGraph_t* bodies) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  cudaError_t e = cudaStreamGetCaptureInfo(cs, &st, nullptr, &g, &deps, &nd);
+  if (e != cudaSuccess) return e;
+  if (st != cudaStreamCaptureStatusActive) return cudaErrorStreamCaptureInvalidated;
+  cudaGraphNodeParams np = {cudaGraphNodeTypeConditional};
+  np.conditional.handle = h;
+  np.conditional.type = type;
+  np.conditional.size = size;
+  cudaGraphNode_t node;
+  e = cudaGraphAddNode(&node, g, deps, nd, &np);
+  if (e != cudaSuccess) return e;
+  for (unsigned i = 0; i < size; ++i) bodies[i] = np.conditional.phGraph_out[i];
+  return cudaStreamUpdateCaptureDependencies(cs, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+// kernels of Arnoldi step j (as in dcgs_cycle; every step of a body starts unconverged)
+static rsfde_status capture_arnoldi_step(rsfde_ctx* c, int j, double tol, const GraphCond& gc, cudaStream_t s) {
+  const long long NP = c->geo.NP;
+  const int nb = reduction_blocks(NP, c->nblk);
+  const double vb = 8.0 * (double)NP;
+  const int* skip = reinterpret_cast<const int*>(c->d_state);  // breakdown inside the step (finish_a)
+  const double* const* Vp = (const double* const*)c->V.data();
+  c->skip = nullptr;
+  TRY(apply_K(c, RSFDE_FORM_A, 0, c->V[j], c->d_vscale + j, c->Z, s));
+  LAUNCH(PC_DOTS, vb * (j + 2), launch_dcgs_dots(Vp, j, c->Z, c->d_part, NP, c->nblk, nullptr, s), "dcgs dots");
+  CKL(launch_dcgs_finish_a(c->d_state, c->d_part, nb, j, c->d_vscale, nullptr, s), "dcgs finish a");
+  LAUNCH(PC_UPD, vb * (j + 2 + (j > 0 ? 2 : 1)), launch_dcgs_update(Vp, j, c->d_state, c->Z, c->d_nrm, NP, c->nblk, skip, s),
+         "dcgs update");
+  CKL(launch_dcgs_finish_b(c->d_state, c->d_nrm, nb, j, tol, c->d_vscale, skip, s, gc), "dcgs finish b");
+  return RSFDE_OK;
+}
+
+static rsfde_status graph_build(rsfde_ctx* c, int restart, int max_iters, int fixed, double tol) {
+  graph_destroy(c);
+  for (int i = 0; i < 2; ++i)
+    if (!c->cap_s[i]) CK(cudaStreamCreateWithFlags(&c->cap_s[i], cudaStreamNonBlocking), "capture stream");
+  if (!c->d_ab) TRY(dalloc(c, (void**)&c->d_ab, 2 * sizeof(double)));
+  int nsteps = restart < max_iters ? restart : max_iters;
+  if (fixed > 0 && fixed < nsteps) nsteps = fixed;
+  auto& G = c->sg;
+  CK(cudaGraphCreate(&G.graph, 0), "graph create");
+  cudaGraphConditionalHandle hc, hk;
+  CK(cudaGraphConditionalHandleCreate(&hc, G.graph, 0, cudaGraphCondAssignDefault), "cond handle");
+  CK(cudaGraphConditionalHandleCreate(&hk, G.graph, 0, cudaGraphCondAssignDefault), "cond handle");
+  GraphCond gc;
+  gc.h_cont = hc;
+  gc.on = 1;
+  const long long NP = c->geo.NP;
+  const int nb = reduction_blocks(NP, c->nblk);
+  const long long l0 = c->launches;
+  const bool prof = c->profiling;
+  c->profiling = 0;
+  c->ab_dev = true;
+  rsfde_status st = RSFDE_OK;
+  cudaGraph_t ifb = nullptr;
+  std::vector<cudaGraph_t> sw(nsteps + 1, nullptr);
+  auto end_capture = [&](cudaStream_t cs) -> rsfde_status {
+    cudaGraph_t out = nullptr;
+    CK(cudaStreamEndCapture(cs, &out), "end capture");
+    return RSFDE_OK;
+  };
+  auto body = [&]() -> rsfde_status {
+    // top level: r0 = P_hat^{-1}(H FH - 2 S_alpha x0), ||r0||, IF step 0 [, IF step 1 ...], SWITCH k
+    cudaStream_t cs = c->cap_s[0];
+    CK(cudaStreamBeginCaptureToGraph(cs, G.graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed), "begin capture");
+    {
+      ChainArgs a;
+      a.xmode = X_INPUT;
+      a.Xin = c->FH;
+      a.R = c->X;
+      a.etafac = -2.0;
+      a.m = 0;
+      a.spectral = true;
+      a.spec = SPEC_PHAT;
+      const cudaStream_t s = cs;
+      rsfde_status r = oper_chain(c, a, c->V[0], s);
+      if (r == RSFDE_OK) {
+        LAUNCH(7, 0, launch_sumsq(c->V[0], c->d_nrm, NP, c->nblk, s), "sumsq");
+        LAUNCH(7, 0, launch_gmres_init(c->d_state, c->d_nrm, nb, c->d_vscale, 1, s, gc), "gmres init");
+      }
+      if (r != RSFDE_OK) {
+        cudaGraph_t junk;
+        cudaStreamEndCapture(cs, &junk);
+        return r;
+      }
+    }
+    G.launches_pre = c->launches - l0;
+    CK(add_cond(cs, hc, cudaGraphCondTypeIf, 1, &ifb), "if node");
+    CK(launch_graph_set_k(c->d_state, hk, cs), "set k");
+    G.launches_pre += 1;
+    CK(add_cond(cs, hk, cudaGraphCondTypeSwitch, (unsigned)(nsteps + 1), sw.data()), "switch node");
+    TRY(end_capture(cs));
+    // Arnoldi steps
+    cudaStream_t bs = c->cap_s[1];
+    cudaGraph_t cur = ifb;
+    for (int j = 0; j < nsteps; ++j) {
+      const long long lj = c->launches;
+      // the IF node of step j+1 sits in step j's body with a handle owned by that body graph, set by
+      // step j's dcgs_finish_b (0 for the last step: nothing to gate)
+      GraphCond gj = gc;
+      cudaGraphConditionalHandle hn = 0;
+      if (j + 1 < nsteps) CK(cudaGraphConditionalHandleCreate(&hn, cur, 0, cudaGraphCondAssignDefault), "cond handle");
+      gj.h_cont = hn;
+      CK(cudaStreamBeginCaptureToGraph(bs, cur, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed), "begin capture");
+      rsfde_status r = capture_arnoldi_step(c, j, tol, gj, bs);
+      if (r != RSFDE_OK) {
+        cudaGraph_t junk;
+        cudaStreamEndCapture(bs, &junk);
+        return r;
+      }
+      cudaGraph_t next = nullptr;
+      if (j + 1 < nsteps) CK(add_cond(bs, hn, cudaGraphCondTypeIf, 1, &next), "nested if node");
+      TRY(end_capture(bs));
+      G.launches_step.push_back(c->launches - lj);
+      cur = next;
+    }
+    // y solve and x update for each final column count k (k = 0: r0 == 0, nothing to do)
+    G.launches_end.push_back(0);
+    {
+      cudaGraphNode_t en;  // (k = 0 body: no work)
+      CK(cudaGraphAddEmptyNode(&en, sw[0], nullptr, 0), "empty node");
+    }
+    for (int k = 1; k <= nsteps; ++k) {
+      const long long lk = c->launches;
+      CK(cudaStreamBeginCaptureToGraph(bs, sw[k], nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed), "begin capture");
+      const double* const* Vp = (const double* const*)c->V.data();
+      const double* d_y =
+          reinterpret_cast<const double*>(reinterpret_cast<const char*>(c->d_state) + offsetof(GmresState, y));
+      const cudaStream_t s = bs;
+      LAUNCH(7, 0, launch_gmres_solve_y(c->d_state, k, s), "solve y");
+      LAUNCH(PC_XUPD, 8.0 * (double)NP * (k + 2), launch_axpy_basis(Vp, c->d_vscale, k, d_y, c->X, NP, s), "x update");
+      TRY(end_capture(bs));
+      G.launches_end.push_back(c->launches - lk);
+    }
+    return RSFDE_OK;
+  };
+  st = body();
+  c->ab_dev = false;
+  c->profiling = prof;
+  c->launches = l0;
+  if (st != RSFDE_OK) {
+    graph_destroy(c);
+    return st;
+  }
+  CK(cudaGraphInstantiate(&G.exec, G.graph, 0), "graph instantiate");
+  G.restart = restart;
+  G.max_iters = max_iters;
+  G.fixed = fixed;
+  G.tol = tol;
+  G.nsteps = nsteps;
+  return RSFDE_OK;
+}
+
+// run the captured first cycle of step m; *steps = Arnoldi steps executed, *fl = final flags
+static rsfde_status gmres_graph_cycle(rsfde_ctx* c, int m, int restart, int max_iters, int fixed, double tol,
+                                      cudaStream_t s, int* steps, Flags* fl) {
+  auto& G = c->sg;
+  if (!G.exec || G.restart != restart || G.max_iters != max_iters || G.fixed != fixed || G.tol != tol)
+    TRY(graph_build(c, restart, max_iters, fixed, tol));
+  if (c->ekind != RSFDE_COEF_GRID) CKL(launch_set_ab(c->d_ab, c->a_half[m], c->b_half[m], s), "set ab");
+  CK(cudaGraphLaunch(G.exec, s), "graph launch");
+  c->graph_replays++;
+  char* h = reinterpret_cast<char*>(c->h_flags);
+  CK(cudaMemcpyAsync(h, c->d_state, sizeof(Flags), cudaMemcpyDeviceToHost, s), "flags copy");
+  CK(cudaMemcpyAsync(h + 48, reinterpret_cast<const char*>(c->d_state) + offsetof(GmresState, kcols), 2 * sizeof(int),
+                     cudaMemcpyDeviceToHost, s),
+     "flags copy");
+  CK(cudaStreamSynchronize(s), "stream sync");
+  memcpy(fl, h, sizeof(Flags));
+  int kk[2];
+  memcpy(kk, h + 48, sizeof kk);
+  const int kcols = kk[0] < 0 ? 0 : kk[0];
+  *steps = kk[1];
+  // kernels the replay launched (the captured launches of the executed bodies)
+  long long n = G.launches_pre;
+  for (int j = 0; j < *steps && j < (int)G.launches_step.size(); ++j) n += G.launches_step[j];
+  if (kcols < (int)G.launches_end.size()) n += G.launches_end[kcols];
+  c->launches += n;
+  return RSFDE_OK;
+}
+
 // GMRES on K x = P^{-1} b with x = c->X on entry (x0) and exit.
 // mode_fast: first-cycle r0 = P_hat^{-1}(H FH - 2 S_alpha x0) with FH = H^{-1} tau F (valid iff
 // x0 = u^{(m)}: b - A u = tau F - 2 S_alpha u, Eq.(tls)); later cycles use b (computed on demand).
@@ -504,6 +720,15 @@ static rsfde_status gmres_core(rsfde_ctx* c, int m, bool mode_fast, bool have_b,
   Flags fl{0, 0, 1.0};
   bool converged = false;
   while (true) {
+    if (first && c->ortho == ORTHO_DCGS2 && graph_eligible(c, form, mode_fast)) {
+      int k = 0;
+      TRY(gmres_graph_cycle(c, m, restart, max_iters, fixed, tol, s, &k, &fl));
+      total += k;
+      converged = fixed > 0 ? (total >= fixed || fl.breakdown != 0) : (fl.converged != 0 || fl.breakdown != 0);
+      if (converged || total >= max_iters) break;
+      first = false;
+      continue;
+    }
     if (form == RSFDE_FORM_TWO_SIDED) {
       // residual of the physical iterate u = P^{-1/2} u~ (X holds u on the first cycle, u~ later)
       if (!have_b) {
@@ -696,6 +921,8 @@ long long rsfde_launch_count(const rsfde_ctx* c, int reset) {
   return v;
 }
 
+long long rsfde_graph_replays(const rsfde_ctx* c) { return c ? c->graph_replays : 0; }
+
 int rsfde_profile(rsfde_ctx* c, int enable) {
   if (!c) return -1;
   cudaDeviceSynchronize();
@@ -723,6 +950,9 @@ int rsfde_profile_read(rsfde_ctx* c, int cls, long long* launches, double* ms, d
 void rsfde_destroy(rsfde_ctx* c) {
   if (!c) return;
   cudaDeviceSynchronize();
+  graph_destroy(c);
+  for (cudaStream_t cs : c->cap_s)
+    if (cs) cudaStreamDestroy(cs);
   for (void* p : c->allocs) cudaFree(p);
   if (c->d_on_F) cudaFree(c->d_on_F);
   if (c->h_flags) cudaFreeHost(c->h_flags);

@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         // X channel from the stage (job 1) into the pair buffer (x = X, or e o R), then
         // y = H X + eta T R on j = g + G m with the stencil neighbours from the buffer
         const PencilConsts kc = (LAST && p.xmode == X_E_TIMES_R) ? make_consts(p, pc, true, false) : kc0;
+        const double2 eab = e_ab(p.e);
         if (p.xmode != X_ZERO) mbar_wait(&full_bar, (unsigned)(job & 1));
         TTRACE(11)
         __syncwarp();
@@ -409,10 +410,10 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
               double2 e;
               if (e_tab) {
                 const double ga = e_ga[j - 1], ka = e_ka[j - 1];
-                e = make_double2(fma(p.e.b * kc.eP_p, ga, p.e.a) + (kc.eK_p + ka),
-                                 fma(p.e.b * kc.eP_q, ga, p.e.a) + (kc.eK_q + ka));
+                e = make_double2(fma(eab.y * kc.eP_p, ga, eab.x) + (kc.eK_p + ka),
+                                 fma(eab.y * kc.eP_q, ga, eab.x) + (kc.eK_q + ka));
               } else {
-                e = e_pair(p, pc, kc, j);
+                e = e_pair(p, pc, kc, j, eab);
               }
               x = make_double2(rs * x.x * e.x, rs * x.y * e.y);
             }

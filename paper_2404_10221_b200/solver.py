@@ -223,6 +223,10 @@ class RsfdeSolver:
     def launch_count(self, reset=False) -> int:
         return int(self.lib.rsfde_launch_count(self.ctx, 1 if reset else 0))
 
+    def graph_replays(self) -> int:
+        """Replays of the graph-captured first GMRES cycle since setup (rsfde_graph_replays)."""
+        return int(self.lib.rsfde_graph_replays(self.ctx))
+
     def device_bytes(self) -> int:
         return int(self.lib.rsfde_device_bytes(self.ctx))
 

@@ -154,9 +154,11 @@ def test_gmres_step_parity(cache, kind, shape):
 
 
 # ----------------------------------------------------------------------- T6 time march
-def _march(prob, restart=None, tol=None, form=0, host=False):
+def _march(prob, restart=None, tol=None, form=0, host=False, solver_out=None):
     from paper_2404_10221_b200 import _lib as L
     S = _solver(prob)
+    if solver_out is not None:
+        solver_out.append(S)
     restart = restart or prob.restart
     tol = tol or prob.tol
     u0 = prob.psi_interior()
@@ -425,3 +427,52 @@ def test_dcgs2_matches_cgs2_and_oracle(name, monkeypatch):
     if r_d["iters"] != ro.iters:
         uo, ro, _ = scheme.solve(prob, F_static=Fst, fixed_iters=r_d["iters"])
     assert relerr(u_d, uo) < 1e-9
+
+
+# ----------------------------------------------------------------------- graph-captured cycles
+@pytest.mark.parametrize("name", ["c5s", "c2s", "ex2", "c4s_r3"])
+def test_graph_cycle_bit_identical_to_stream_path(name, monkeypatch):
+    # the first GMRES cycle of each CN step runs as one CUDA graph (r0, Arnoldi steps as conditional
+    # IF nodes gated on the device convergence flag, SWITCH on the column count for y and x += V y):
+    # the same kernels in the same order as the stream path (RSFDE_NO_GRAPH=1), so iteration counts
+    # and solutions agree bit for bit; with restart 3 the later cycles of a step continue on the
+    # stream path from the graph's state
+    prob = {"c5s": lambda: I.config_c5(M=4, nn=(31, 15, 63)),
+            "c2s": lambda: I.config_c2(n=63, M=6),
+            "ex2": lambda: I.example(2, 31, 8, (1.5, 1.7)),
+            "c4s_r3": lambda: I.config_c4(n=31, M=3)}[name]()
+    restart = 3 if name.endswith("_r3") else None
+    ss = []
+    u_g, r_g = _march(prob, restart=restart, solver_out=ss)
+    assert ss[0].graph_replays() == prob.M, ss[0].graph_replays()
+    monkeypatch.setenv("RSFDE_NO_GRAPH", "1")
+    ss = []
+    u_s, r_s = _march(prob, restart=restart, solver_out=ss)
+    assert ss[0].graph_replays() == 0
+    monkeypatch.delenv("RSFDE_NO_GRAPH")
+    assert r_g["iters"] == r_s["iters"], (r_g["iters"], r_s["iters"])
+    assert np.array_equal(u_g, u_s)
+    assert list(r_g["relres"]) == list(r_s["relres"])
+    Fst = scheme.source_F(prob, 0) if prob.source_static else None
+    uo, ro, _ = scheme.solve(prob, F_static=Fst, restart=restart)
+    assert max(abs(a - b) for a, b in zip(r_g["iters"], ro.iters)) <= 1
+    if r_g["iters"] != ro.iters:
+        uo, ro, _ = scheme.solve(prob, F_static=Fst, restart=restart, fixed_iters=r_g["iters"])
+    assert relerr(u_g, uo) < 1e-9
+
+
+def test_graph_cycle_replay_mode_and_zero_residual():
+    # fixed_iters (replay) caps the captured IF chain; a zero right-hand side converges at r0 = 0
+    # with no Arnoldi step and no x update
+    prob = I.config_c5(M=2, nn=(15, 7, 31))
+    S = _solver(prob)
+    F = S.compact_source(_dev(prob.f_closed(prob.t_half(0))))
+    u = _dev(prob.psi_interior())
+    rep = S.solve_steps(u, F=F, F_static=True, cfg=S.cfg(restart=prob.restart, fixed_iters=3))
+    assert rep["iters"] == [3, 3] and S.graph_replays() == 2
+    Fst = scheme.source_F(prob, 0)
+    uo, ro, _ = scheme.solve(prob, F_static=Fst, fixed_iters=[3, 3])
+    assert relerr(_host(u), uo) < 1e-9
+    z = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
+    rep = S.solve_steps(z, F=torch.zeros_like(F), F_static=True, cfg=S.cfg(restart=prob.restart, tol=prob.tol))
+    assert rep["iters"] == [0, 0] and all(rep["converged"]) and float(z.abs().max()) == 0.0
