@@ -171,6 +171,28 @@ __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* s
 // conflict-free across the 8 buffers
 __device__ __forceinline__ int oswz(int k, int w) { return k ^ (w & 7); }
 
+// Strided axes: the staged outputs of the tile's pairs (pair buffers, k = 1..n at oswz(k, q)) leave as
+// whole tile rows.  The compute thread count is a multiple of TP, so a thread always serves the same
+// pair column q and rows row0, row0 + RSTEP, ...: no index division, one validity load, one pointer
+// increment per row.
+template <int TP, int CW, int L, int kN>
+__device__ __forceinline__ void coop_store_rows(const double2* bufs, const int* tvalid, double* out, long long base,
+                                                long long stride) {
+  constexpr int RSTEP = 32 * CW / TP;
+  const int q = threadIdx.x % TP, row0 = threadIdx.x / TP;
+  const int vm = tvalid[q];
+  if (!(vm & 1) || (RSFDE_TILE_SKIP & 2)) return;
+  const double2* src = bufs + q * L;
+  double* dst = out + base + (long long)row0 * stride + 2 * q;
+  const long long dstep = (long long)RSTEP * stride;
+#pragma unroll 4
+  for (int row = row0; row < kN; row += RSTEP, dst += dstep) {
+    const double2 c = src[oswz(row + 1, q)];
+    if (vm & 2) *reinterpret_cast<double2*>(dst) = c;
+    else *dst = c.x;
+  }
+}
+
 template <int MODE, class T, int TP, bool CT>
 __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg<TP * T::G / 32>::kCtasPerSm)
     tile_kernel(const PassParams p, const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmX) {
@@ -224,6 +246,9 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   // (last axis: the same arrays hold the spectrum tables lambda^H_k and tq_k of the axis)
   __shared__ double e_ga[N], e_ka[N];
   const bool e_tab = OPER && p.xmode == X_E_TIMES_R && p.e.kind != 2;
+  // e(x, t) constant along the pass axis (no axis factor g_a, k_a: e.g. C5's e(x1, t) on the x3 pass):
+  // X = E o R is R times a per-pencil constant, so the stencil reads R straight from the stage
+  const bool e_const = e_tab && !p.e.g[p.axis] && !p.e.k[p.axis];
   if (e_tab) {
     const double* ga = p.e.g[p.axis];
     const double* ka = p.e.k[p.axis];
@@ -323,16 +348,18 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
       if (OPER && ph == 0) {
         // C = S H R = s lambda^H D(R) (non-last spectral pass), via the partner spectrum
         if (!LAST) {
+          // only the upper half is read back (the partner L - k of a lower k >= 1 is >= N + 1)
           __syncwarp();
 #pragma unroll
-          for (int r = 0; r < E; ++r) buf[T::rowk(g, r)] = v[r];
+          for (int r = 0; r < E; ++r)
+            if (!T::lower(r)) buf[T::rowk(g, r)] = v[r];
           __syncwarp();
           double2 cv[E / 2];
 #pragma unroll
           for (int r = 0, i = 0; r < E; ++r) {
             if (!T::lower(r)) continue;
             const int k = T::rowk(g, r);
-            const double2 zm = buf[(L - k) & (L - 1)];
+            const double2 zm = (k >= 1) ? buf[L - k] : make_double2(0.0, 0.0);
             const double f = (k >= 1) ? crs * __ldg(p.lamH + k - 1) : 0.0;
             cv[i++] = make_double2(-(v[r].y - zm.y) * f, (v[r].x - zm.x) * f);
           }
@@ -365,17 +392,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             __syncwarp();
           } else {
             compute_bar<CW>();
-            const long long base = tile_base<TP, NH, CT>(p, t);
-            for (int e = threadIdx.x; e < kN * kTilePairs; e += kComputeThreads) {
-              const int row = e / kTilePairs, q = e % kTilePairs;
-              const double2 c = bufs[q * L + oswz(row + 1, q)];
-              const int vm = tvalid[q];
-              if (!(vm & 1)) continue;
-              double* dst = p.C + base + (long long)row * p.stride + 2 * q;
-              if (RSFDE_TILE_SKIP & 2) continue;
-              if (vm & 2) *reinterpret_cast<double2*>(dst) = c;
-              else *dst = c.x;
-            }
+            coop_store_rows<TP, CW, L, kN>(bufs, tvalid, p.C, tile_base<TP, NH, CT>(p, t), p.stride);
             compute_bar<CW>();
           }
           }  // RSFDE_TILE_COOP_STORES
@@ -399,6 +416,47 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         const double2 eab = e_ab(p.e);
         if (p.xmode != X_ZERO) mbar_wait(&full_bar, (unsigned)(job & 1));
         TTRACE(11)
+        if (p.xmode == X_INPUT || e_const) {
+          // X is an input vector (or R times a pencil constant): the stencil neighbours come straight
+          // from the stage (3 shared loads per value instead of a load, a store to the pair buffer and
+          // 3 loads); invalid pencils are masked on y (their stage values are finite: zero pads or TMA
+          // zero fill)
+          if (p.xmode == X_INPUT) {
+#pragma unroll
+            for (int m = 0; m < E / 2; ++m) {
+              const int j = g + G * m;
+              double2 y = make_double2(0.0, 0.0);
+              if (j >= 1 && j <= kN) {
+                const double2 x0 = stage_pair<TP, NH, CT>(p, stage, w, j);
+                const double2 xl = (j > 1) ? stage_pair<TP, NH, CT>(p, stage, w, j - 1) : make_double2(0.0, 0.0);
+                const double2 xn = (j < kN) ? stage_pair<TP, NH, CT>(p, stage, w, j + 1) : make_double2(0.0, 0.0);
+                y.x = pc.vp ? fma(hc0s, x0.x, fma(hc1s, xl.x + xn.x, etas * v[m].x)) : 0.0;
+                y.y = pc.vq ? fma(hc0s, x0.y, fma(hc1s, xl.y + xn.y, etas_y * v[m].y)) : 0.0;
+              }
+              v[m] = y;
+            }
+          } else {
+            // e = a + b eP + eK on the whole pencil (the axis factors are 1 and 0)
+            const double sp = rs * (fma(eab.y * kc.eP_p, 1.0, eab.x) + kc.eK_p);
+            const double sq = rs * (fma(eab.y * kc.eP_q, 1.0, eab.x) + kc.eK_q);
+#pragma unroll
+            for (int m = 0; m < E / 2; ++m) {
+              const int j = g + G * m;
+              double2 y = make_double2(0.0, 0.0);
+              if (j >= 1 && j <= kN) {
+                const double2 x0 = stage_pair<TP, NH, CT>(p, stage, w, j);
+                const double2 xl = (j > 1) ? stage_pair<TP, NH, CT>(p, stage, w, j - 1) : make_double2(0.0, 0.0);
+                const double2 xn = (j < kN) ? stage_pair<TP, NH, CT>(p, stage, w, j + 1) : make_double2(0.0, 0.0);
+                y.x = pc.vp ? fma(sp, fma(hc0s, x0.x, hc1s * (xl.x + xn.x)), etas * v[m].x) : 0.0;
+                y.y = pc.vq ? fma(sq, fma(hc0s, x0.y, hc1s * (xl.y + xn.y)), etas_y * v[m].y) : 0.0;
+              }
+              v[m] = y;
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar);
+          ++job;
+        } else {
         __syncwarp();
 #pragma unroll
         for (int m = 0; m < E / 2; ++m) {
@@ -441,6 +499,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           }
           v[m] = y;
         }
+        }  // X_INPUT
         TTRACE(10)
         odd_extend<T>(v, buf, g);
       } else if (ph == 2 && LAST) {
@@ -532,17 +591,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           __syncwarp();
         } else {
           compute_bar<CW>();
-          const long long base = tile_base<TP, NH, CT>(p, t);
-          for (int e = threadIdx.x; e < kN * kTilePairs; e += kComputeThreads) {
-            const int row = e / kTilePairs, q = e % kTilePairs;
-            const int vm = tvalid[q];
-            if (!(vm & 1)) continue;
-            const double2 yv = bufs[q * L + oswz(row + 1, q)];
-            double* dst = p.Y + base + (long long)row * p.stride + 2 * q;
-            if (RSFDE_TILE_SKIP & 2) continue;
-              if (vm & 2) *reinterpret_cast<double2*>(dst) = yv;
-            else *dst = yv.x;
-          }
+          coop_store_rows<TP, CW, L, kN>(bufs, tvalid, p.Y, tile_base<TP, NH, CT>(p, t), p.stride);
           compute_bar<CW>();
         }
         }  // RSFDE_TILE_COOP_STORES

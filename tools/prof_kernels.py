@@ -1,8 +1,8 @@
 """Run the hot operator chain in isolation for ncu: warm-up K = P_hat^{-1} A (3 spectral operator
 passes + 2 inverse DST passes) once, then the same chain again (the profiled launches).
 
-    python tools/prof_kernels.py [n] [reps]
-ncu: -k regex:"oper_pass|dst_pass" -s 5 -c 5  captures the second chain.
+    python tools/prof_kernels.py [n] [reps] [--cfg C3]
+ncu: -k regex:"oper_pass|dst_pass" -s 5 -c 5  captures the second chain (3D; a 2D chain is 3 launches).
 """
 import os
 import sys
@@ -19,9 +19,14 @@ if "--lib" in sys.argv:  # experiment variant of the library (tools/tile_variant
     i = sys.argv.index("--lib")
     L.load(sys.argv[i + 1])
     del sys.argv[i:i + 2]
+cfg = "C5"
+if "--cfg" in sys.argv:  # another BASELINE config at its full size (C2, C3, C4)
+    i = sys.argv.index("--cfg")
+    cfg = sys.argv[i + 1]
+    del sys.argv[i:i + 2]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 511
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-prob = I.config_c5(n=n)
+prob = I.config_c5(n=n) if cfg == "C5" else {"C2": I.config_c2, "C3": I.config_c3, "C4": I.config_c4}[cfg]()
 S = RsfdeSolver.from_problem(prob)
 x = torch.from_numpy(I.seeded_vector(1, prob.n)).cuda()
 y = torch.empty_like(x)
