@@ -167,6 +167,37 @@ __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* s
   return *reinterpret_cast<const double2*>(stage + (size_t)r * kRowBytes + ((w ^ sw) << 4));
 }
 
+// Stage column of pair w for the axis positions j = j0 + G m (m = 0, 1, ...): the swizzle chunk of a
+// strided stage row r depends on r mod 8 only (r & 7, or (r >> 1) & 3), which G m (G = 16, 32) does not
+// change, so one base pointer per thread serves every m (constant offsets m G kRowBytes); contiguous
+// stage: element (r & 255) of box (r >> 8) of pencil 2w / 2w + 1.  Valid for j0 - 1 + G m in 0..NH-1.
+template <int TP, int NH, bool CT, int G>
+struct StageCol {
+  const char* base;
+  __device__ __forceinline__ StageCol(const char* stage, int w, int j0) {
+    RSFDE_TILE_CONSTS
+    const int r = j0 - 1;
+    if (CT) {
+      base = stage + (size_t)((2 * w) * kBoxRows) * 8;  // (r handled in at())
+      r0 = r;
+    } else {
+      const int sw = kTilePairs == 8 ? (r & 7) : ((r >> 1) & 3);
+      base = stage + (ptrdiff_t)r * kRowBytes + ((w ^ sw) << 4);
+      r0 = 0;
+    }
+  }
+  int r0;
+  __device__ __forceinline__ double2 at(int m) const {
+    RSFDE_TILE_CONSTS
+    if (CT) {
+      const int r = r0 + G * m;
+      const double* s = reinterpret_cast<const double*>(base) + (r >> 8) * (kTilePencils * kBoxRows) + (r & 255);
+      return make_double2(s[0], s[kBoxRows]);
+    }
+    return *reinterpret_cast<const double2*>(base + (ptrdiff_t)m * G * kRowBytes);
+  }
+};
+
 // XOR swizzle of the per-pair output buffers so that the cooperative row stores read
 // conflict-free across the 8 buffers
 __device__ __forceinline__ int oswz(int k, int w) { return k ^ (w & 7); }
@@ -363,7 +394,21 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             const double f = (k >= 1) ? crs * __ldg(p.lamH + k - 1) : 0.0;
             cv[i++] = make_double2(-(v[r].y - zm.y) * f, (v[r].x - zm.x) * f);
           }
-          if (!RSFDE_TILE_COOP_STORES) {
+          if (CT && E == G) {
+            // contiguous axis: row register r holds k = g + G r, so a warp's stores of one r are 32
+            // consecutive doubles of each pencil -- coalesced straight from registers, no staging
+            double* cp = p.C + pc.off_p + (g - 1);  // k - 1 = (g - 1) + G r: constant offsets per r
+            double* cq = p.C + pc.off_q + (g - 1);
+#pragma unroll
+            for (int r = 0, i = 0; r < E; ++r) {
+              if (!T::lower(r)) continue;
+              if ((r > 0 || g > 0) && !(RSFDE_TILE_SKIP & 2)) {
+                if (pc.vp) cp[G * r] = cv[i].x;
+                if (pc.vq) cq[G * r] = cv[i].y;
+              }
+              ++i;
+            }
+          } else if (!RSFDE_TILE_COOP_STORES) {
             // store C straight from registers: 16-byte (pencil pair) pieces per row on strided axes
             // (the neighbouring pairs' warps fill the rest of each row piece at the same time; L2
             // merges the sectors), coalesced 8-byte elements on the contiguous axis
@@ -422,14 +467,15 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           // 3 loads); invalid pencils are masked on y (their stage values are finite: zero pads or TMA
           // zero fill)
           if (p.xmode == X_INPUT) {
+            const StageCol<TP, NH, CT, G> c0(stage, w, g), cl(stage, w, g - 1), cn(stage, w, g + 1);
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const int j = g + G * m;
               double2 y = make_double2(0.0, 0.0);
               if (j >= 1 && j <= kN) {
-                const double2 x0 = stage_pair<TP, NH, CT>(p, stage, w, j);
-                const double2 xl = (j > 1) ? stage_pair<TP, NH, CT>(p, stage, w, j - 1) : make_double2(0.0, 0.0);
-                const double2 xn = (j < kN) ? stage_pair<TP, NH, CT>(p, stage, w, j + 1) : make_double2(0.0, 0.0);
+                const double2 x0 = c0.at(m);
+                const double2 xl = (j > 1) ? cl.at(m) : make_double2(0.0, 0.0);
+                const double2 xn = (j < kN) ? cn.at(m) : make_double2(0.0, 0.0);
                 y.x = pc.vp ? fma(hc0s, x0.x, fma(hc1s, xl.x + xn.x, etas * v[m].x)) : 0.0;
                 y.y = pc.vq ? fma(hc0s, x0.y, fma(hc1s, xl.y + xn.y, etas_y * v[m].y)) : 0.0;
               }
@@ -439,14 +485,15 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             // e = a + b eP + eK on the whole pencil (the axis factors are 1 and 0)
             const double sp = rs * (fma(eab.y * kc.eP_p, 1.0, eab.x) + kc.eK_p);
             const double sq = rs * (fma(eab.y * kc.eP_q, 1.0, eab.x) + kc.eK_q);
+            const StageCol<TP, NH, CT, G> c0(stage, w, g), cl(stage, w, g - 1), cn(stage, w, g + 1);
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const int j = g + G * m;
               double2 y = make_double2(0.0, 0.0);
               if (j >= 1 && j <= kN) {
-                const double2 x0 = stage_pair<TP, NH, CT>(p, stage, w, j);
-                const double2 xl = (j > 1) ? stage_pair<TP, NH, CT>(p, stage, w, j - 1) : make_double2(0.0, 0.0);
-                const double2 xn = (j < kN) ? stage_pair<TP, NH, CT>(p, stage, w, j + 1) : make_double2(0.0, 0.0);
+                const double2 x0 = c0.at(m);
+                const double2 xl = (j > 1) ? cl.at(m) : make_double2(0.0, 0.0);
+                const double2 xn = (j < kN) ? cn.at(m) : make_double2(0.0, 0.0);
                 y.x = pc.vp ? fma(sp, fma(hc0s, x0.x, hc1s * (xl.x + xn.x)), etas * v[m].x) : 0.0;
                 y.y = pc.vq ? fma(sq, fma(hc0s, x0.y, hc1s * (xl.y + xn.y)), etas_y * v[m].y) : 0.0;
               }
@@ -567,7 +614,19 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         }
       } else {
         // final DST (row layout) -> Y
-        if (!RSFDE_TILE_COOP_STORES) {
+        if (CT && E == G) {
+          // contiguous axis: coalesced stores straight from the row registers (see the C output)
+          double* yp = p.Y + pc.off_p + (g - 1);
+          double* yq = p.Y + pc.off_q + (g - 1);
+#pragma unroll
+          for (int r = 0; r < E; ++r) {
+            if (!T::lower(r)) continue;
+            if ((r > 0 || g > 0) && !(RSFDE_TILE_SKIP & 2)) {
+              if (pc.vp) yp[G * r] = -v[r].y;
+              if (pc.vq) yq[G * r] = v[r].x;
+            }
+          }
+        } else if (!RSFDE_TILE_COOP_STORES) {
 #pragma unroll
           for (int r = 0; r < E; ++r) {
             if (!T::lower(r)) continue;
