@@ -554,6 +554,45 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         // loop over the same k (small code: the spectrum kinds are a runtime switch)
         const PencilConsts ks = make_consts(p, pc, false, true);
         const Spec& S = p.spec;
+        const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
+        const double icHp = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / ks.cH_p) * hs;  // (hs of the inverse DST)
+        const double icHq = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / ks.cH_q) * hs;
+        bool done = false;
+        if constexpr (E == G) {
+          if (fast && !e_tab) {
+            // row register m holds k = g + G m, which is also column index j = g + G m of this thread:
+            // the scaled values stay in registers and only the mirror half of the odd extension of the
+            // second DST passes through the pair buffer
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < E / 2; ++m) {
+              const int k = g + G * m;
+              double2 wv = make_double2(0.0, 0.0);
+              if (k >= 1) {
+                const double lh = (S.kind == SPEC_PALPHA) ? 1.0 : e_ga[k - 1];
+                double lp = 1.0, lq = 1.0;
+                if (S.kind != SPEC_HINV) {
+                  const double tq = e_ka[k - 1];
+                  lp = S.ebar + ks.cP_p + tq;
+                  lq = S.ebar + ks.cP_q + tq;
+                }
+                wv.x = pc.vp ? -v[m].y * (rcp_nr(lp * lh) * icHp) : 0.0;
+                wv.y = pc.vq ? v[m].x * (rcp_nr(lq * lh) * icHq) : 0.0;
+              }
+              v[m] = wv;
+              buf[k] = wv;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int m = E / 2; m < E; ++m) {
+              const int j = g + G * m;
+              const double2 tt = (j == N) ? make_double2(0.0, 0.0) : buf[L - j];
+              v[m] = make_double2(-tt.x, -tt.y);
+            }
+            done = true;
+          }
+        }
+        if (!done) {
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < E; ++r) {
@@ -563,9 +602,6 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         __syncwarp();  // (E > G: the loop below reads k values written by other threads of the group)
         // Lambda = (ebar + cP + tq_k) cH lh_k (P_hat) | (ebar + cP + tq_k) (P_alpha) | cH lh_k (H):
         // one fast reciprocal per value instead of an IEEE division
-        const bool fast = S.kind == SPEC_PHAT || S.kind == SPEC_PALPHA || S.kind == SPEC_HINV;
-        const double icHp = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / ks.cH_p) * hs;  // (hs of the inverse DST)
-        const double icHq = ((S.kind == SPEC_PALPHA) ? 1.0 : 1.0 / ks.cH_q) * hs;
         if (fast && !e_tab) {
           // unrolled: the 16 values are independent (a rolled loop serialises the latencies)
 #pragma unroll
@@ -612,6 +648,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             v[m] = make_double2(-tt.x, -tt.y);
           }
         }
+        }  // !done
       } else {
         // final DST (row layout) -> Y
         if (CT && E == G) {
