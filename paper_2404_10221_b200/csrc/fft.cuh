@@ -133,6 +133,27 @@ __device__ __forceinline__ int xidx(int k1, int t) {
 
 // Forward FFT, column layout in -> row layout out.  buf: L double2 of shared memory owned
 // by this group.  Caller guarantees nobody else is reading buf (a __syncwarp precedes).
+// (split in two halves so that a caller can wait for its exchange buffer between them: the first
+// half touches registers only)
+template <int E, int G>
+__device__ __forceinline__ void fft_fwd_pre(double2 (&v)[E], int g, const double2* __restrict__ tw) {
+  dft<E>(v);
+  twiddle_col<E, false>(v, tw, g, E * G);
+}
+template <int E, int G>
+__device__ __forceinline__ void fft_fwd_post(double2 (&v)[E], double2* buf, int g) {
+  constexpr int R = E / G;
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < E; ++k1) buf[xidx<E, G>(k1, g)] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int ri = 0; ri < R; ++ri)
+#pragma unroll
+    for (int t = 0; t < G; ++t) v[ri * G + t] = buf[xidx<E, G>(g * R + ri, t)];
+#pragma unroll
+  for (int ri = 0; ri < R; ++ri) dft<G>(v + ri * G);
+}
 template <int E, int G>
 __device__ __forceinline__ void fft_fwd(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw) {
   constexpr int R = E / G;

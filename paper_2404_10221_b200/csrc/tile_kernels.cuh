@@ -100,6 +100,18 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 }
 template <int CW>
 __device__ __forceinline__ void compute_bar() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * CW) : "memory"); }
+// Strided tiles hand their staged outputs to the three spare warps of the producer warpgroup (the
+// "store warps"): named barrier 2 = outputs staged (compute warps arrive, store warps wait), 3 = pair
+// buffers free again (store warps arrive, compute warps wait right before their next buffer write).
+constexpr int kStoreWarps = 3;
+template <int CW>
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "n"(32 * (CW + kStoreWarps)) : "memory");
+}
+template <int CW>
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "n"(32 * (CW + kStoreWarps)) : "memory");
+}
 
 // element offset of the first pencil of tile t (strided: pencil 16t; contiguous: row 16t)
 template <int TP, int NH, bool CT>
@@ -206,11 +218,12 @@ __device__ __forceinline__ int oswz(int k, int w) { return k ^ (w & 7); }
 // whole tile rows.  The compute thread count is a multiple of TP, so a thread always serves the same
 // pair column q and rows row0, row0 + RSTEP, ...: no index division, one validity load, one pointer
 // increment per row.
-template <int TP, int CW, int L, int kN>
+template <int TP, int NT, int L, int kN>
 __device__ __forceinline__ void coop_store_rows(const double2* bufs, const int* tvalid, double* out, long long base,
-                                                long long stride) {
-  constexpr int RSTEP = 32 * CW / TP;
-  const int q = threadIdx.x % TP, row0 = threadIdx.x / TP;
+                                                long long stride, int tid) {
+  constexpr int RSTEP = NT / TP;
+  static_assert(NT % TP == 0, "store threads must be a multiple of the tile width");
+  const int q = tid % TP, row0 = tid / TP;
   const int vm = tvalid[q];
   if (!(vm & 1) || (RSFDE_TILE_SKIP & 2)) return;
   const double2* src = bufs + q * L;
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   double2* bufs = reinterpret_cast<double2*>(tsm);                        // TP x L x 16 bytes
   char* stage = tsm + (size_t)kTilePairs * L * sizeof(double2);           // 1024-aligned
   __shared__ __align__(8) unsigned long long full_bar, empty_bar;
-  __shared__ int tvalid[kTilePairs];  // validity bits (p, q) of each pair in the current tile
+  __shared__ int tvalid[2][kTilePairs];  // validity bits (p, q) of each pair, by tile parity (store warps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long ntiles = CT ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
   const int jobs_per_tile = OPER ? (p.xmode == X_ZERO ? 1 : 2) : 1;
@@ -257,7 +270,24 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
 
   if (warp >= CW) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
-    if (warp != CW) return;
+    if (warp != CW) {
+      if (CT || warp > CW + kStoreWarps) return;
+      // -------------------------------------------------------------- store warps (strided tiles)
+      const int sid = threadIdx.x - 32 * (CW + 1);
+      int tc = 0;
+      for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc) {
+        const long long base = tile_base<TP, NH, CT>(p, t);
+        if (OPER && !LAST) {
+          named_sync<CW>(2);
+          coop_store_rows<TP, 32 * kStoreWarps, L, kN>(bufs, tvalid[tc & 1], p.C, base, p.stride, sid);
+          named_arrive<CW>(3);
+        }
+        named_sync<CW>(2);
+        coop_store_rows<TP, 32 * kStoreWarps, L, kN>(bufs, tvalid[tc & 1], p.Y, base, p.stride, sid);
+        named_arrive<CW>(3);
+      }
+      return;
+    }
     // ------------------------------------------------------------------ producer warp
     long long job = 0;
     for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -310,7 +340,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   const double etas_y = (E == G) ? -etas : etas;
   long long job = 0;
   int tcount = 0;
-  (void)tcount;
+  bool pend_free = false;  // staged outputs handed to the store warps, pair buffers not yet released
 #if RSFDE_TILE_TRACE
   const int trace_launch = *(volatile int*)&g_trace_launch;
 #endif
@@ -318,7 +348,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     const long long pair = (long long)kTilePairs * t + w;
     const bool active = pair < p.npairs;
     const PairCtx pc = make_pair(p, active ? pair : 0, active);
-    if (g == 0) tvalid[w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
+    if (g == 0) tvalid[tcount & 1][w] = (pc.vp ? 1 : 0) | (pc.vq ? 2 : 0);
     // per-pencil constants of e(x,t): their table loads are issued here, at the tile start, so that
     // their latency hides behind the first FFT (not in the last-axis kernel, where the live
     // registers would spill; the last-axis spectrum constants are loaded where they are used)
@@ -354,7 +384,13 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar);
     ++job;
-    if (!OPER) odd_extend<T>(v, buf, g);
+    if (!OPER) {
+      if (!CT && pend_free) {  // the previous tile's staged outputs may still be read by the store warps
+        named_sync<CW>(3);
+        pend_free = false;
+      }
+      odd_extend<T>(v, buf, g);
+    }
 
     const int first = OPER ? 0 : 2;
     const int last_phase = LAST ? 3 : 2;
@@ -370,8 +406,17 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         if constexpr (E == G) {
           // phase 1 (the convolution's inverse FFT) is conj(FFT(conj(.))): the input conj is folded
           // into the spectrum scaling of phase 0 and the output conj into the stencil of phase 1
-          fft_fwd<E, G>(v, buf, g, p.tw);
+          fft_fwd_pre<E, G>(v, g, p.tw);
+          if (!CT && pend_free) {  // the register-only first half overlaps the store warps' copy
+            named_sync<CW>(3);
+            pend_free = false;
+          }
+          fft_fwd_post<E, G>(v, buf, g);
         } else {
+          if (!CT && pend_free) {
+            named_sync<CW>(3);
+            pend_free = false;
+          }
           T::fft(v, buf, g, p.tw, ph == 1);  // E = R G: forward and inverse differ in layout
         }
       }
@@ -436,9 +481,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             }
             __syncwarp();
           } else {
-            compute_bar<CW>();
-            coop_store_rows<TP, CW, L, kN>(bufs, tvalid, p.C, tile_base<TP, NH, CT>(p, t), p.stride);
-            compute_bar<CW>();
+            named_arrive<CW>(2);  // the store warps write C out while the next FFT starts
+            pend_free = true;
           }
           }  // RSFDE_TILE_COOP_STORES
         }
@@ -686,9 +730,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           }
           __syncwarp();
         } else {
-          compute_bar<CW>();
-          coop_store_rows<TP, CW, L, kN>(bufs, tvalid, p.Y, tile_base<TP, NH, CT>(p, t), p.stride);
-          compute_bar<CW>();
+          named_arrive<CW>(2);  // the store warps write Y out during the next tile's first FFT
+          pend_free = true;
         }
         }  // RSFDE_TILE_COOP_STORES
       }
