@@ -18,7 +18,8 @@ static int tile_pairs(const PassParams& p) {
   // RSFDE_TILE128=1 forces them on every eligible strided pass (test coverage at small sizes).
   const char* f128 = getenv("RSFDE_TILE128");
   const bool force128 = f128 && strcmp(f128, "0");
-  if (p.inner % 16 == 0 && (force128 || p.stride * 8 >= (1ll << 20))) return 8;
+  const bool force64 = f128 && !strcmp(f128, "0");  // (experiments: 64-byte tiles everywhere)
+  if (p.inner % 16 == 0 && !force64 && (force128 || p.stride * 8 >= (1ll << 20))) return 8;
   return p.inner % 8 == 0 ? 4 : 0;
 }
 

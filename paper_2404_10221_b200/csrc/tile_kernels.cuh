@@ -259,7 +259,11 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   __shared__ int tvalid[2][kTilePairs];  // validity bits (p, q) of each pair, by tile parity (store warps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long ntiles = CT ? ((p.geo.NP / p.geo.P) + kTilePencils - 1) / kTilePencils : (p.npairs + kTilePairs - 1) / kTilePairs;
-  const int jobs_per_tile = OPER ? (p.xmode == X_ZERO ? 1 : 2) : 1;
+  // e(x, t) constant along the pass axis (no axis factor g_a, k_a: e.g. C5's e(x1, t) on the x3 pass):
+  // X = E o R is R times a per-pencil constant, so the stencil reads R from the stage of job 0, which
+  // stays resident until then (one load of R per tile instead of two)
+  const bool single_R = OPER && p.xmode == X_E_TIMES_R && p.e.kind != 2 && !p.e.g[p.axis] && !p.e.k[p.axis];
+  const int jobs_per_tile = OPER ? ((p.xmode == X_ZERO || single_R) ? 1 : 2) : 1;
   if (skip_launch(p.skip)) return;  // speculative launch after convergence (uniform over the grid)
   if (threadIdx.x == 0) {
     mbar_init(&full_bar, 1);
@@ -307,9 +311,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   // (last axis: the same arrays hold the spectrum tables lambda^H_k and tq_k of the axis)
   __shared__ double e_ga[N], e_ka[N];
   const bool e_tab = OPER && p.xmode == X_E_TIMES_R && p.e.kind != 2;
-  // e(x, t) constant along the pass axis (no axis factor g_a, k_a: e.g. C5's e(x1, t) on the x3 pass):
-  // X = E o R is R times a per-pencil constant, so the stencil reads R straight from the stage
-  const bool e_const = e_tab && !p.e.g[p.axis] && !p.e.k[p.axis];
+  const bool e_const = single_R;
   if (e_tab) {
     const double* ga = p.e.g[p.axis];
     const double* ka = p.e.k[p.axis];
@@ -381,9 +383,11 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         v[m] = r;
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty_bar);
-    ++job;
+    if (!single_R) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar);
+      ++job;
+    }
     if (!OPER) {
       if (!CT && pend_free) {  // the previous tile's staged outputs may still be read by the store warps
         named_sync<CW>(3);
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         // y = H X + eta T R on j = g + G m with the stencil neighbours from the buffer
         const PencilConsts kc = (LAST && p.xmode == X_E_TIMES_R) ? make_consts(p, pc, true, false) : kc0;
         const double2 eab = e_ab(p.e);
-        if (p.xmode != X_ZERO) mbar_wait(&full_bar, (unsigned)(job & 1));
+        if (p.xmode != X_ZERO && !single_R) mbar_wait(&full_bar, (unsigned)(job & 1));
         TTRACE(11)
         if (p.xmode == X_INPUT || e_const) {
           // X is an input vector (or R times a pencil constant): the stencil neighbours come straight
