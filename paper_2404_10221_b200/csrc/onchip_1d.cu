@@ -49,7 +49,7 @@ __host__ __device__ inline OnchipShared onchip_layout(int n, int restart) {
   L.g = o; o += restart + 1;
   L.y = o; o += restart;
   L.red = o; o += 2 * kOnWarps + 8;
-  L.scr = o; o += 4 * n + 4;   // partial row sums of the split dense products
+  L.scr = o; o += 8 * n + 8;   // partial row sums of the split dense products
   L.total = o;
   return L;
 }
@@ -69,10 +69,8 @@ __device__ __forceinline__ double on_block_sum(double v, double* red) {
   __syncthreads();
   if (lane == 0) red[wp] = v;
   __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < kOnWarps; ++i) s += red[i];
-  return s;
+  // every warp reduces the kOnWarps partials with shuffles (one load per lane instead of 32 per thread)
+  return on_warp_sum(lane < kOnWarps ? red[lane] : 0.0);
 }
 
 struct OnchipCtx {
@@ -82,34 +80,35 @@ struct OnchipCtx {
   int n;
 };
 
-// dense row sums out_i = sum_j coef(i, j) in_j with up to 4 threads per row (partial sums in scr)
-template <class Coef>
-__device__ __forceinline__ void on_rowsum(const OnchipCtx& C, const double* in, Coef coef, int jlo, int jhi,
-                                          double* res) {
-  const int n = C.n;
+// out = T in   (T = [s_|i-j|], the FCD Toeplitz matrix).  T is persymmetric (J T J = T), so row n-1-i
+// of T in is row i of T (J in): rows i and n-1-i share every coefficient load.  Up to 8 threads per row
+// pair, each over an eighth of j (partial sums in scr).
+__device__ __forceinline__ void on_toeplitz(const OnchipCtx& C, const double* in, double* out) {
+  const double* s = C.sm + C.L.sgen;
+  const int n = C.n, half = (n + 1) / 2;  // (n + 1 is a power of two: shifts and masks)
   double* scr = C.sm + C.L.scr;
-  const int parts = n <= (int)blockDim.x ? min(4, (int)blockDim.x / n) : 1;
-  const int len = jhi - jlo, chunk = (len + parts - 1) / parts;
-  for (int t = threadIdx.x; t < parts * n; t += blockDim.x) {
-    const int i = t % n, pt = t / n;
-    const int j0 = jlo + pt * chunk, j1 = min(jhi, j0 + chunk);
-    double acc = 0.0;
-    for (int j = j0; j < j1; ++j) acc = fma(coef(i, j), in[j], acc);
-    scr[pt * n + i] = acc;
+  const int lh = __ffs(half) - 1;
+  const int parts = min(8, max(1, (int)blockDim.x >> lh));
+  const int chunk = (n + parts - 1) >> (__ffs(parts) - 1);
+  for (int t = threadIdx.x; t < parts * half; t += blockDim.x) {
+    const int i = t & (half - 1), pt = t >> lh;
+    const int j0 = pt * chunk, j1 = min(n, j0 + chunk);
+    double a1 = 0.0, a2 = 0.0;
+    for (int j = j0; j < j1; ++j) {
+      const double c = s[i > j ? i - j : j - i];
+      a1 = fma(c, in[j], a1);
+      a2 = fma(c, in[n - 1 - j], a2);
+    }
+    scr[pt * n + i] = a1;
+    if (n - 1 - i != i) scr[pt * n + (n - 1 - i)] = a2;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double acc = scr[i];
     for (int pt = 1; pt < parts; ++pt) acc += scr[pt * n + i];
-    res[i] = acc;
+    out[i] = acc;
   }
   __syncthreads();
-}
-
-// out = T in   (T = [s_|i-j|], the FCD Toeplitz matrix)
-__device__ __forceinline__ void on_toeplitz(const OnchipCtx& C, const double* in, double* out) {
-  const double* s = C.sm + C.L.sgen;
-  on_rowsum(C, in, [s](int i, int j) { return s[i > j ? i - j : j - i]; }, 0, C.n, out);
 }
 
 // out = A in  (uses t1, t2)
@@ -130,31 +129,50 @@ __device__ void on_apply_A(const OnchipCtx& C, const double* in, double* out) {
 }
 
 // out = S in (orthonormal DST-I), k = 1..n stored at k-1; sint[i] = sin(pi i/(n+1)), i < 2(n+1).
-// Up to 4 threads per output k, each over a quarter of j.  sin(pi k j/(n+1)) advances by a rotation
-// through the angle pi k/(n+1) from an exact table value at the start of the quarter (a table gather
-// per term would hit the same shared-memory bank for many k at once); <= n/4 rotations keep the
-// recurrence error below ~1e-14 relative.
+// Outputs k and N-k (N = n+1) share their sines: sin(pi j (N-k)/N) = -(-1)^j sin(pi j k/N), so with
+// A_k = sum over even j, B_k = sum over odd j of in_j sin(pi j k/N): out_k = A_k + B_k, out_{N-k} = B_k - A_k
+// (half the sine recurrences of a row-by-row sum).  Up to 8 threads per k <= N/2, each over an eighth of
+// j; sin(pi k j/N) advances by a rotation through pi k/N from an exact table value at the start of the
+// chunk (a table gather per term would hit the same shared-memory bank for many k at once); <= n/8
+// rotations keep the recurrence error below ~1e-15 relative.  N = n + 1 is a power of two (setup), so
+// N is even and sint[i + N/2] = cos(pi i/N).
 __device__ void on_dst(const OnchipCtx& C, const double* in, double* out) {
-  const int n = C.n, N2 = 2 * (n + 1), Q = (n + 1) / 2;  // sint[i + Q] = cos(pi i/(n+1)) (n+1 even)
+  const int n = C.n, N = n + 1, N2 = 2 * N, Q = N / 2;
   const double* st = C.sm + C.L.sint;
   double* scr = C.sm + C.L.scr;
-  const double sc = sqrt(2.0 / (double)(n + 1));
-  const int parts = n <= (int)blockDim.x ? min(4, (int)blockDim.x / n) : 1;
-  const int chunk = (n + parts - 1) / parts;
-  for (int t = threadIdx.x; t < parts * n; t += blockDim.x) {
-    const int k = t % n + 1, pt = t / n;
+  const double sc = sqrt(2.0 / (double)N);
+  const int nk = N / 2;  // k = 1..N/2 computed directly, N-k from the same sums
+  // (N, nk, N2 are powers of two: shifts and masks instead of divisions)
+  const int lk = __ffs(nk) - 1, m2 = N2 - 1;
+  const int parts = min(8, max(1, (int)blockDim.x >> lk));
+  const int chunk = (n + parts - 1) >> (__ffs(parts) - 1);
+  for (int t = threadIdx.x; t < parts * nk; t += blockDim.x) {
+    const int k = (t & (nk - 1)) + 1, pt = t >> lk;
     const int j0 = 1 + pt * chunk, j1 = min(n, j0 + chunk - 1);
-    const int i0 = (int)(((long long)k * j0) % N2);
-    double sv = st[i0], cv = st[(i0 + Q) % N2];
-    const double sd = st[k % N2], cd = st[(k + Q) % N2];
-    double acc = 0.0;
-    for (int j = j0; j <= j1; ++j) {
-      acc = fma(sv, in[j - 1], acc);
+    const int i0 = (k * j0) & m2;
+    double sv = st[i0], cv = st[(i0 + Q) & m2];
+    const double sd = st[k], cd = st[(k + Q) & m2];
+    double aE = 0.0, aO = 0.0;  // sums over even / odd j
+    auto rot = [&]() {
       const double s2 = fma(sv, cd, cv * sd);
       cv = fma(cv, cd, -sv * sd);
       sv = s2;
+    };
+    int j = j0;
+    if (j <= j1 && (j & 1)) {  // align to an even j
+      aO = fma(sv, in[j - 1], aO);
+      rot();
+      ++j;
     }
-    scr[pt * n + (k - 1)] = acc;
+    for (; j + 1 <= j1; j += 2) {
+      aE = fma(sv, in[j - 1], aE);
+      rot();
+      aO = fma(sv, in[j], aO);
+      rot();
+    }
+    if (j <= j1) aE = fma(sv, in[j - 1], aE);
+    scr[pt * n + (k - 1)] = aE + aO;
+    if (N - k != k) scr[pt * n + (N - k - 1)] = aO - aE;
   }
   __syncthreads();
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
