@@ -125,6 +125,12 @@ struct PassParams {
   // global coordinates of this (possibly sharded / transposed) grid: axis i of the local array
   // starts at global index coff[i] of a physical axis with cext[i] interior points; pencils whose
   // global coordinate on a non-pass axis is >= cext are zero pads (never stored)
+  // Segmented contiguous axis (slab-sharded teams, rsfde_shard.cu): with seg_lg > 0 the pencils are the
+  // all-to-all blocks [r][row][x_l] (x = r 2^seg_lg + x_l, row = pencil): element (pencil, position j) at
+  // (x >> seg_lg) seg_stride + pencil 2^seg_lg + (x & (2^seg_lg - 1)), x = j - 1, for every vector of the
+  // pass (the last pass reads the receive buffers and writes the send buffer of the next exchange).
+  int seg_lg;
+  long long seg_stride;
   int coff[3];
   int cext[3];
   // speculative Arnoldi launches: when non-null and skip[0] | skip[1] (the GmresState converged /

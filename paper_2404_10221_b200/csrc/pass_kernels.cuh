@@ -121,8 +121,9 @@ __device__ __forceinline__ PairCtx make_pair(const PassParams& p, long long pair
   if (p.contiguous) {
     const long long rows = G.NP / G.P;
     const long long r0 = 2 * pair, r1 = 2 * pair + 1;
-    pc.off_p = r0 * G.P;
-    pc.off_q = r1 * G.P;
+    const long long rl = p.seg_lg ? (1ll << p.seg_lg) : (long long)G.P;  // pencil (row) length in memory
+    pc.off_p = r0 * rl;
+    pc.off_q = r1 * rl;
     pc.pen_p = r0;
     pc.pen_q = r1 < rows ? r1 : r0;
     pencil_coords(p, pc.pen_p, a0, a1, a2);
@@ -159,12 +160,19 @@ __device__ __forceinline__ PencilConsts make_consts(const PassParams& p, const P
   return k;
 }
 
+// offset of axis position j (1..n) from the pencil base: (j-1) stride, or the segmented contiguous layout
+__device__ __forceinline__ long long pos_off(const PassParams& p, int j) {
+  const int x = j - 1;
+  if (p.seg_lg) return (long long)(x >> p.seg_lg) * p.seg_stride + (x & ((1 << p.seg_lg) - 1));
+  return (long long)x * p.stride;
+}
+
 // value pair at axis position j (1..n); zero outside or for invalid pencils
 __device__ __forceinline__ double2 ld_pair(const PassParams& p, const double* __restrict__ X, const PairCtx& pc,
                                            int j) {
   double2 r = make_double2(0.0, 0.0);
   if (j < 1 || j > p.n) return r;
-  const long long off = (long long)(j - 1) * p.stride;
+  const long long off = pos_off(p, j);
   if (pc.vec2) {
     r = __ldg(reinterpret_cast<const double2*>(X + pc.off_p + off));
   } else {
@@ -176,7 +184,7 @@ __device__ __forceinline__ double2 ld_pair(const PassParams& p, const double* __
 
 __device__ __forceinline__ void st_pair(const PassParams& p, double* X, const PairCtx& pc, int j, double2 v) {
   if (j < 1 || j > p.n) return;
-  const long long off = (long long)(j - 1) * p.stride;
+  const long long off = pos_off(p, j);
   if (pc.vec2) {
     *reinterpret_cast<double2*>(X + pc.off_p + off) = v;
   } else {

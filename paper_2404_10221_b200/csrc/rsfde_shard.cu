@@ -104,8 +104,10 @@ __global__ void pack_TA_kernel(const double* __restrict__ T, double* __restrict_
 }
 
 // recv block r'' (x2 in [r'' s2, ...)) = [x2l][x3][x1l]  ->  A = [x1l][x2 < n2][x3 (+pad)]
+// (planes x1l >= s_real are the x1 pad planes of the last slab: written as zeros -- with fused exchanges
+// the send block position of the pad plane is not written by the x1 pass and holds stale data)
 __global__ void unpack_TA_kernel(const double* __restrict__ recv, double* __restrict__ A, int s, int n2, int n3,
-                                 int P3, int s2, long long blk) {
+                                 int P3, int s2, long long blk, int s_real) {
   __shared__ double tile[32][33];
   const int x2 = blockIdx.z;
   const int x1_0 = blockIdx.x * 32, x3_0 = blockIdx.y * 32;
@@ -118,7 +120,7 @@ __global__ void unpack_TA_kernel(const double* __restrict__ recv, double* __rest
   if (x2 >= n2) return;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int x1l = x1_0 + i, x3 = x3_0 + threadIdx.x;
-    if (x1l < s && x3 < n3) A[((long long)x1l * n2 + x2) * P3 + x3] = tile[threadIdx.x][i];
+    if (x1l < s && x3 < n3) A[((long long)x1l * n2 + x2) * P3 + x3] = x1l < s_real ? tile[threadIdx.x][i] : 0.0;
   }
 }
 
@@ -142,8 +144,9 @@ struct ShardBufs {
   int x1lo = 0, x2lo = 0, s_real = 0;
   double* W[4] = {nullptr, nullptr, nullptr, nullptr};
   double *Z = nullptr, *X = nullptr, *U0 = nullptr, *FP = nullptr, *FH = nullptr, *BUF = nullptr, *TMP = nullptr;
-  double* T[4] = {nullptr, nullptr, nullptr, nullptr};
-  double *send = nullptr, *recv = nullptr;
+  double* T[4] = {nullptr, nullptr, nullptr, nullptr};  // layout T (unfused exchanges only)
+  double* send[3] = {nullptr, nullptr, nullptr};        // all-to-all blocks [r][x2l][x3][x1l], P blk each
+  double* recv[3] = {nullptr, nullptr, nullptr};
   std::vector<double*> V;
   double *vscale = nullptr, *h1 = nullptr, *h2 = nullptr, *part = nullptr, *nrm = nullptr, *red = nullptr;
   GmresState* st = nullptr;
@@ -152,6 +155,9 @@ struct ShardBufs {
 struct rsfde_team {
   rsfde_ctx* tab = nullptr;  // tables of the global problem (no work vectors)
   int P = 1, rank0 = 0, nlocal = 1, s = 0, s2 = 0;
+  // fused exchanges: the x1 passes read the receive blocks and write the send blocks directly
+  // (segmented contiguous axis, PassParams::seg_lg), so only pack A->T and unpack T->A remain
+  bool fused = false;
   long long blk = 0;
   std::vector<ShardBufs> sh;
   ncclComm_t comm = nullptr;
@@ -252,22 +258,27 @@ static ECoef ecoefA(const rsfde_team* t, int m) {
   return e;
 }
 
-// all-to-all of the shards' send buffers into their recv buffers
-static rsfde_status team_alltoall(rsfde_team* t, cudaStream_t s) {
+// all-to-all of the shards' send buffers 0..nv-1 into their recv buffers (one NCCL group for all nv
+// vectors: the two channels of the operator chain travel in one exchange)
+static rsfde_status team_alltoall(rsfde_team* t, cudaStream_t s, int nv = 1) {
   const size_t bytes = (size_t)t->blk * sizeof(double);
   if (!t->comm) {
-    for (int dst = 0; dst < t->P; ++dst)
-      for (int src = 0; src < t->P; ++src)
-        TCK(cudaMemcpyAsync(t->sh[dst].recv + (long long)src * t->blk, t->sh[src].send + (long long)dst * t->blk, bytes,
-                            cudaMemcpyDeviceToDevice, s),
-            "alltoall copy");
+    for (int v = 0; v < nv; ++v)
+      for (int dst = 0; dst < t->P; ++dst)
+        for (int src = 0; src < t->P; ++src)
+          TCK(cudaMemcpyAsync(t->sh[dst].recv[v] + (long long)src * t->blk, t->sh[src].send[v] + (long long)dst * t->blk,
+                              bytes, cudaMemcpyDeviceToDevice, s),
+              "alltoall copy");
     return RSFDE_OK;
   }
   TNC(g_nccl.GroupStart(), "ncclGroupStart");
-  for (int peer = 0; peer < t->P; ++peer) {
-    TNC(g_nccl.Send(t->sh[0].send + (long long)peer * t->blk, (size_t)t->blk, ncclDouble, peer, t->comm, s), "ncclSend");
-    TNC(g_nccl.Recv(t->sh[0].recv + (long long)peer * t->blk, (size_t)t->blk, ncclDouble, peer, t->comm, s), "ncclRecv");
-  }
+  for (int v = 0; v < nv; ++v)
+    for (int peer = 0; peer < t->P; ++peer) {
+      TNC(g_nccl.Send(t->sh[0].send[v] + (long long)peer * t->blk, (size_t)t->blk, ncclDouble, peer, t->comm, s),
+          "ncclSend");
+      TNC(g_nccl.Recv(t->sh[0].recv[v] + (long long)peer * t->blk, (size_t)t->blk, ncclDouble, peer, t->comm, s),
+          "ncclRecv");
+    }
   TNC(g_nccl.GroupEnd(), "ncclGroupEnd");
   return RSFDE_OK;
 }
@@ -291,14 +302,14 @@ static rsfde_status transpose_AT(rsfde_team* t, double* const* srcA, double* con
     const ShardBufs& b = t->sh[l];
     const int n2 = t->tab->n[1], n3 = t->tab->n[2];
     dim3 grid((n3 + 31) / 32, (t->s + 31) / 32, t->P * t->s2);
-    TCKL((pack_AT_kernel<<<grid, dim3(32, 8), 0, s>>>(srcA[l], b.send, t->s, n2, n3, b.gA.P, t->s2, t->blk),
+    TCKL((pack_AT_kernel<<<grid, dim3(32, 8), 0, s>>>(srcA[l], b.send[0], t->s, n2, n3, b.gA.P, t->s2, t->blk),
           cudaGetLastError()),
          "pack A->T");
   }
   TTRY(team_alltoall(t, s));
   for (int l = 0; l < t->nlocal; ++l) {
     const ShardBufs& b = t->sh[l];
-    TCKL((unpack_AT_kernel<<<stream_blocks(), 256, 0, s>>>(b.recv, dstT[l], t->s, t->s2, t->tab->n[2], b.gT.P, t->blk),
+    TCKL((unpack_AT_kernel<<<stream_blocks(), 256, 0, s>>>(b.recv[0], dstT[l], t->s, t->s2, t->tab->n[2], b.gT.P, t->blk),
           cudaGetLastError()),
          "unpack A->T");
   }
@@ -308,7 +319,7 @@ static rsfde_status transpose_AT(rsfde_team* t, double* const* srcA, double* con
 static rsfde_status transpose_TA(rsfde_team* t, double* const* srcT, double* const* dstA, cudaStream_t s) {
   for (int l = 0; l < t->nlocal; ++l) {
     const ShardBufs& b = t->sh[l];
-    TCKL((pack_TA_kernel<<<stream_blocks(), 256, 0, s>>>(srcT[l], b.send, t->s, t->s2, t->tab->n[2], b.gT.P, t->P, t->blk),
+    TCKL((pack_TA_kernel<<<stream_blocks(), 256, 0, s>>>(srcT[l], b.send[0], t->s, t->s2, t->tab->n[2], b.gT.P, t->P, t->blk),
           cudaGetLastError()),
          "pack T->A");
   }
@@ -317,11 +328,48 @@ static rsfde_status transpose_TA(rsfde_team* t, double* const* srcT, double* con
     const ShardBufs& b = t->sh[l];
     const int n2 = t->tab->n[1], n3 = t->tab->n[2];
     dim3 grid((t->s + 31) / 32, (n3 + 31) / 32, t->P * t->s2);
-    TCKL((unpack_TA_kernel<<<grid, dim3(32, 8), 0, s>>>(b.recv, dstA[l], t->s, n2, n3, b.gA.P, t->s2, t->blk),
+    TCKL((unpack_TA_kernel<<<grid, dim3(32, 8), 0, s>>>(b.recv[0], dstA[l], t->s, n2, n3, b.gA.P, t->s2, t->blk, b.s_real),
           cudaGetLastError()),
          "unpack T->A");
   }
   return RSFDE_OK;
+}
+
+// fused exchanges: pack layout-A vectors into send buffers 0..nv-1 (one group), exchange
+static rsfde_status pack_send_AT(rsfde_team* t, const std::vector<std::vector<const double*>>& srcA, cudaStream_t s) {
+  const int nv = (int)srcA.size();
+  for (int v = 0; v < nv; ++v)
+    for (int l = 0; l < t->nlocal; ++l) {
+      const ShardBufs& b = t->sh[l];
+      const int n2 = t->tab->n[1], n3 = t->tab->n[2];
+      dim3 grid((n3 + 31) / 32, (t->s + 31) / 32, t->P * t->s2);
+      TCKL((pack_AT_kernel<<<grid, dim3(32, 8), 0, s>>>(srcA[v][l], b.send[v], t->s, n2, n3, b.gA.P, t->s2, t->blk),
+            cudaGetLastError()),
+           "pack A->T");
+    }
+  return team_alltoall(t, s, nv);
+}
+// ... and after the x1 pass wrote its send blocks: exchange, unpack into layout A
+static rsfde_status exchange_unpack_TA(rsfde_team* t, double* const* dstA, cudaStream_t s) {
+  TTRY(team_alltoall(t, s, 1));
+  for (int l = 0; l < t->nlocal; ++l) {
+    const ShardBufs& b = t->sh[l];
+    const int n2 = t->tab->n[1], n3 = t->tab->n[2];
+    dim3 grid((t->s + 31) / 32, (n3 + 31) / 32, t->P * t->s2);
+    TCKL((unpack_TA_kernel<<<grid, dim3(32, 8), 0, s>>>(b.recv[0], dstA[l], t->s, n2, n3, b.gA.P, t->s2, t->blk, b.s_real),
+          cudaGetLastError()),
+         "unpack T->A");
+  }
+  return RSFDE_OK;
+}
+// x1-pass parameters on the receive blocks (segmented contiguous axis: segments of s planes)
+static PassParams paramsT_seg(const rsfde_team* t, int l) {
+  PassParams p = paramsT(t, l);
+  int lg = 0;
+  while ((1 << lg) < t->s) ++lg;
+  p.seg_lg = lg;
+  p.seg_stride = t->blk;
+  return p;
 }
 
 struct TChain {
@@ -364,13 +412,41 @@ static rsfde_status team_chain(rsfde_team* t, const TChain& a, double* const* ou
     p.C = b.W[3];
     TCKL(launch_oper_pass(p, a.spectral, false, s), "pass x2");
   }
+  const bool addB = !a.spectral && !a.B.empty() && a.B[0];
+  if (t->fused) {
+    // both channels (and B) in one exchange; the x1 pass reads the receive blocks and writes the send
+    // blocks of the way back
+    std::vector<std::vector<const double*>> src(addB ? 3 : 2, std::vector<const double*>(nl));
+    for (int l = 0; l < nl; ++l) {
+      src[0][l] = t->sh[l].W[2];
+      src[1][l] = t->sh[l].W[3];
+      if (addB) src[2][l] = a.B[l];
+    }
+    TTRY(pack_send_AT(t, src, s));
+    for (int l = 0; l < nl; ++l) {
+      ShardBufs& b = t->sh[l];
+      PassParams p = paramsT_seg(t, l);
+      p.xmode = X_INPUT;
+      p.X = b.recv[0];
+      p.R = b.recv[1];
+      p.eta = a.etafac * t->tab->eta[0];
+      p.spec.kind = a.spec;
+      p.ycoef = a.ycoef;
+      p.B = addB ? b.recv[2] : nullptr;
+      p.bcoef = a.bcoef;
+      p.Y = b.send[0];
+      TCKL(launch_oper_pass(p, a.spectral, true, s), "pass x1");
+    }
+    std::vector<double*> dstA(nl);
+    for (int l = 0; l < nl; ++l) dstA[l] = a.spectral ? t->sh[l].W[0] : out[l];
+    TTRY(exchange_unpack_TA(t, dstA.data(), s));
+  } else {
   // transpose both channels (and B) to layout T
   std::vector<double*> srcA(nl), dstT(nl);
   for (int l = 0; l < nl; ++l) { srcA[l] = t->sh[l].W[2]; dstT[l] = t->sh[l].T[0]; }
   TTRY(transpose_AT(t, srcA.data(), dstT.data(), s));
   for (int l = 0; l < nl; ++l) { srcA[l] = t->sh[l].W[3]; dstT[l] = t->sh[l].T[1]; }
   TTRY(transpose_AT(t, srcA.data(), dstT.data(), s));
-  const bool addB = !a.spectral && !a.B.empty() && a.B[0];
   if (addB) {
     for (int l = 0; l < nl; ++l) { srcA[l] = const_cast<double*>(a.B[l]); dstT[l] = t->sh[l].T[2]; }
     TTRY(transpose_AT(t, srcA.data(), dstT.data(), s));
@@ -396,6 +472,7 @@ static rsfde_status team_chain(rsfde_team* t, const TChain& a, double* const* ou
     dstA[l] = a.spectral ? t->sh[l].W[0] : out[l];
   }
   TTRY(transpose_TA(t, srcT.data(), dstA.data(), s));
+  }  // unfused
   if (!a.spectral) return RSFDE_OK;
   // inverse DSTs along x2 and x3 (layout A)
   for (int l = 0; l < nl; ++l) {
@@ -427,6 +504,21 @@ static rsfde_status team_precond(rsfde_team* t, int kind, double* const* in, dou
     TCKL(launch_dst_pass(q, false, s), "dst x2");
   }
   std::vector<double*> srcA(nl), dstT(nl), srcT(nl), dstA(nl);
+  if (t->fused) {
+    std::vector<std::vector<const double*>> src(1, std::vector<const double*>(nl));
+    for (int l = 0; l < nl; ++l) src[0][l] = t->sh[l].W[1];
+    TTRY(pack_send_AT(t, src, s));
+    for (int l = 0; l < nl; ++l) {
+      ShardBufs& b = t->sh[l];
+      PassParams p = paramsT_seg(t, l);
+      p.X = b.recv[0];
+      p.Y = b.send[0];
+      p.spec.kind = kind;
+      TCKL(launch_dst_pass(p, true, s), "dst x1 (scaled)");
+    }
+    for (int l = 0; l < nl; ++l) dstA[l] = t->sh[l].W[0];
+    TTRY(exchange_unpack_TA(t, dstA.data(), s));
+  } else {
   for (int l = 0; l < nl; ++l) { srcA[l] = t->sh[l].W[1]; dstT[l] = t->sh[l].T[0]; }
   TTRY(transpose_AT(t, srcA.data(), dstT.data(), s));
   for (int l = 0; l < nl; ++l) {
@@ -439,6 +531,7 @@ static rsfde_status team_precond(rsfde_team* t, int kind, double* const* in, dou
   }
   for (int l = 0; l < nl; ++l) { srcT[l] = t->sh[l].T[3]; dstA[l] = t->sh[l].W[0]; }
   TTRY(transpose_TA(t, srcT.data(), dstA.data(), s));
+  }
   for (int l = 0; l < nl; ++l) {
     ShardBufs& b = t->sh[l];
     PassParams p = paramsA(t, l, 1);
@@ -728,6 +821,12 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
   t->s = (n1 + 1) / nranks;
   t->s2 = (n2 + 1) / nranks;
   t->blk = (long long)t->s2 * n3 * t->s;
+  // fused exchanges need segments of at most 256 planes (one TMA box per tile: nranks >= 2 at n1 = 511);
+  // RSFDE_TEAM_UNFUSED=1 keeps the explicit layout-T transposes (test comparison)
+  {
+    const char* uf = getenv("RSFDE_TEAM_UNFUSED");
+    t->fused = nranks >= 2 && t->s <= 256 && !(uf && *uf && strcmp(uf, "0"));
+  }
   t->sh.resize(nlocal);
   auto fail = [&](rsfde_status e) {
     g_team_error = t->err;
@@ -758,10 +857,13 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     double** va[] = {&b.W[0], &b.W[1], &b.W[2], &b.W[3], &b.Z, &b.X, &b.U0, &b.FP, &b.FH, &b.BUF, &b.TMP};
     for (double** v : va)
       if ((st = talloc(t, v, (size_t)b.gA.NP)) != RSFDE_OK) return fail(st);
-    for (int i = 0; i < 4; ++i)
-      if ((st = talloc(t, &b.T[i], (size_t)b.gT.NP)) != RSFDE_OK) return fail(st);
-    if ((st = talloc(t, &b.send, (size_t)(nranks * t->blk))) != RSFDE_OK) return fail(st);
-    if ((st = talloc(t, &b.recv, (size_t)(nranks * t->blk))) != RSFDE_OK) return fail(st);
+    if (!t->fused)
+      for (int i = 0; i < 4; ++i)
+        if ((st = talloc(t, &b.T[i], (size_t)b.gT.NP)) != RSFDE_OK) return fail(st);
+    for (int v = 0; v < (t->fused ? 3 : 1); ++v) {
+      if ((st = talloc(t, &b.send[v], (size_t)(nranks * t->blk))) != RSFDE_OK) return fail(st);
+      if ((st = talloc(t, &b.recv[v], (size_t)(nranks * t->blk))) != RSFDE_OK) return fail(st);
+    }
     double** sm[] = {&b.vscale, &b.h1, &b.h2, &b.red};
     for (double** v : sm)
       if ((st = talloc(t, v, 128)) != RSFDE_OK) return fail(st);  // (DCGS2: 2j+2 <= 100 sums)

@@ -143,7 +143,10 @@ __device__ __forceinline__ void produce(const PassParams& p, const CUtensorMap* 
                                         unsigned long long* full) {
   RSFDE_TILE_CONSTS
   mbar_expect_tx(full, (unsigned)kStageBytes);
-  if (CT) {
+  if (CT && p.seg_lg) {
+    // segmented rows (all-to-all blocks): one box {2^seg_lg, pencils, segments} -> stage [seg][pencil][x_l]
+    tma_load_3d(stage, tm, 0, (int)(kTilePencils * t), 0, full);
+  } else if (CT) {
 #pragma unroll
     for (int b = 0; b < kNBox; ++b)
       tma_load_3d(stage + (size_t)b * (kStageBytes / kNBox), tm, b * kBoxRows, (int)(kTilePencils * t), 0, full);
@@ -170,9 +173,10 @@ template <int TP, int NH, bool CT>
 __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* stage, int w, int j) {
   RSFDE_TILE_CONSTS
   const int r = j - 1;
-  if (CT) {
-    const double* s = reinterpret_cast<const double*>(stage) + (r >> 8) * (kTilePencils * kBoxRows) + (r & 255);
-    return make_double2(s[(2 * w) * kBoxRows], s[(2 * w + 1) * kBoxRows]);
+  if (CT) {  // stage [r >> lg][pencil][r & (2^lg - 1)], lg = 8 (two 256-row boxes) or the segment length
+    const int lg = p.seg_lg ? p.seg_lg : 8;
+    const double* s = reinterpret_cast<const double*>(stage) + (r >> lg) * (kTilePencils << lg) + (r & ((1 << lg) - 1));
+    return make_double2(s[(2 * w) << lg], s[(2 * w + 1) << lg]);
   }
   // 128-byte swizzle: 16-byte chunk c of row r at c ^ (r & 7); 64-byte swizzle: c ^ ((r >> 1) & 3)
   const int sw = kTilePairs == 8 ? (r & 7) : ((r >> 1) & 3);
@@ -186,11 +190,12 @@ __device__ __forceinline__ double2 stage_pair(const PassParams& p, const char* s
 template <int TP, int NH, bool CT, int G>
 struct StageCol {
   const char* base;
-  __device__ __forceinline__ StageCol(const char* stage, int w, int j0) {
+  __device__ __forceinline__ StageCol(const PassParams& p, const char* stage, int w, int j0) {
     RSFDE_TILE_CONSTS
     const int r = j0 - 1;
     if (CT) {
-      base = stage + (size_t)((2 * w) * kBoxRows) * 8;  // (r handled in at())
+      lg = p.seg_lg ? p.seg_lg : 8;
+      base = stage + (size_t)((2 * w) << lg) * 8;  // (r handled in at())
       r0 = r;
     } else {
       const int sw = kTilePairs == 8 ? (r & 7) : ((r >> 1) & 3);
@@ -198,13 +203,13 @@ struct StageCol {
       r0 = 0;
     }
   }
-  int r0;
+  int r0, lg;
   __device__ __forceinline__ double2 at(int m) const {
     RSFDE_TILE_CONSTS
     if (CT) {
       const int r = r0 + G * m;
-      const double* s = reinterpret_cast<const double*>(base) + (r >> 8) * (kTilePencils * kBoxRows) + (r & 255);
-      return make_double2(s[0], s[kBoxRows]);
+      const double* s = reinterpret_cast<const double*>(base) + (r >> lg) * (kTilePencils << lg) + (r & ((1 << lg) - 1));
+      return make_double2(s[0], s[1 << lg]);
     }
     return *reinterpret_cast<const double2*>(base + (ptrdiff_t)m * G * kRowBytes);
   }
@@ -452,8 +457,14 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             for (int r = 0, i = 0; r < E; ++r) {
               if (!T::lower(r)) continue;
               if ((r > 0 || g > 0) && !(RSFDE_TILE_SKIP & 2)) {
-                if (pc.vp) cp[G * r] = cv[i].x;
-                if (pc.vq) cq[G * r] = cv[i].y;
+                if (p.seg_lg) {
+                  const long long o = pos_off(p, g + G * r);
+                  if (pc.vp) p.C[pc.off_p + o] = cv[i].x;
+                  if (pc.vq) p.C[pc.off_q + o] = cv[i].y;
+                } else {
+                  if (pc.vp) cp[G * r] = cv[i].x;
+                  if (pc.vq) cq[G * r] = cv[i].y;
+                }
               }
               ++i;
             }
@@ -480,8 +491,9 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             for (int j = g + 1; j <= kN; j += G) {
               const double2 c = buf[oswz(j, w)];
               if (RSFDE_TILE_SKIP & 2) continue;
-              if (pc.vp) p.C[pc.off_p + j - 1] = c.x;
-              if (pc.vq) p.C[pc.off_q + j - 1] = c.y;
+              const long long o = pos_off(p, j);
+              if (pc.vp) p.C[pc.off_p + o] = c.x;
+              if (pc.vq) p.C[pc.off_q + o] = c.y;
             }
             __syncwarp();
           } else {
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           // 3 loads); invalid pencils are masked on y (their stage values are finite: zero pads or TMA
           // zero fill)
           if (p.xmode == X_INPUT) {
-            const StageCol<TP, NH, CT, G> c0(stage, w, g), cl(stage, w, g - 1), cn(stage, w, g + 1);
+            const StageCol<TP, NH, CT, G> c0(p, stage, w, g), cl(p, stage, w, g - 1), cn(p, stage, w, g + 1);
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const int j = g + G * m;
@@ -533,7 +545,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             // e = a + b eP + eK on the whole pencil (the axis factors are 1 and 0)
             const double sp = rs * (fma(eab.y * kc.eP_p, 1.0, eab.x) + kc.eK_p);
             const double sq = rs * (fma(eab.y * kc.eP_q, 1.0, eab.x) + kc.eK_q);
-            const StageCol<TP, NH, CT, G> c0(stage, w, g), cl(stage, w, g - 1), cn(stage, w, g + 1);
+            const StageCol<TP, NH, CT, G> c0(p, stage, w, g), cl(p, stage, w, g - 1), cn(p, stage, w, g + 1);
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const int j = g + G * m;
@@ -707,8 +719,14 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           for (int r = 0; r < E; ++r) {
             if (!T::lower(r)) continue;
             if ((r > 0 || g > 0) && !(RSFDE_TILE_SKIP & 2)) {
-              if (pc.vp) yp[G * r] = -v[r].y;
-              if (pc.vq) yq[G * r] = v[r].x;
+              if (p.seg_lg) {  // (the send blocks of the next all-to-all)
+                const long long o = pos_off(p, g + G * r);
+                if (pc.vp) p.Y[pc.off_p + o] = -v[r].y;
+                if (pc.vq) p.Y[pc.off_q + o] = v[r].x;
+              } else {
+                if (pc.vp) yp[G * r] = -v[r].y;
+                if (pc.vq) yq[G * r] = v[r].x;
+              }
             }
           }
         } else if (!RSFDE_TILE_COOP_STORES) {
@@ -729,8 +747,9 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           for (int j = g + 1; j <= kN; j += G) {
             const double2 yv = buf[oswz(j, w)];
             if (RSFDE_TILE_SKIP & 2) continue;
-            if (pc.vp) p.Y[pc.off_p + j - 1] = yv.x;
-            if (pc.vq) p.Y[pc.off_q + j - 1] = yv.y;
+            const long long o = pos_off(p, j);
+            if (pc.vp) p.Y[pc.off_p + o] = yv.x;
+            if (pc.vq) p.Y[pc.off_q + o] = yv.y;
           }
           __syncwarp();
         } else {
@@ -768,7 +787,15 @@ static cudaError_t tile_tensor_map(const PassParams& p, const double* X, CUtenso
   cuuint64_t dims[3], strides[2];
   cuuint32_t box[3], es[3] = {1, 1, 1};
   CUtensorMapSwizzle swz;
-  if (p.contiguous) {
+  if (p.contiguous && p.seg_lg) {
+    // segmented rows: {x_l < 2^seg_lg, pencil, segment}, segment stride seg_stride; one box per tile
+    const long long S = 1ll << p.seg_lg;
+    dims[0] = (cuuint64_t)S; dims[1] = (cuuint64_t)(p.geo.NP / p.geo.P); dims[2] = (cuuint64_t)(NH / S);
+    strides[0] = (cuuint64_t)S * 8; strides[1] = (cuuint64_t)p.seg_stride * 8;
+    box[0] = (cuuint32_t)S; box[1] = kTilePencils; box[2] = (cuuint32_t)(NH / S);
+    if (S > 256 || NH % S) return cudaErrorInvalidValue;
+    swz = CU_TENSOR_MAP_SWIZZLE_NONE;
+  } else if (p.contiguous) {
     dims[0] = (cuuint64_t)p.geo.P; dims[1] = (cuuint64_t)(p.geo.NP / p.geo.P); dims[2] = 1;
     strides[0] = dims[0] * 8; strides[1] = dims[0] * dims[1] * 8;
     box[0] = kBoxRows; box[1] = kTilePencils; box[2] = 1;

@@ -103,3 +103,33 @@ def test_slab_compact_source():
         assert lo == 8 * l and cnt == min(8, 31 - lo)
         got = _host(T.compact_source(_dev(f[lo:lo + cnt + 2]), local=l))
         assert relerr(got, ref[lo:lo + cnt]) < 1e-14
+
+
+@pytest.mark.parametrize("shape,P", [((511, 15, 31), 2), ((255, 31, 63), 4), ((255, 15, 31), 8), ((31, 15, 63), 2)])
+def test_fused_exchanges_equal_explicit_transposes(shape, P, monkeypatch):
+    # fused exchanges (the x1 passes read the receive blocks and write the send blocks directly:
+    # segmented contiguous axis) against the explicit layout-T transposes (RSFDE_TEAM_UNFUSED=1):
+    # the same arithmetic, so the K chain, the preconditioner and a march agree bit for bit
+    from paper_2404_10221_b200 import _lib as L
+    from paper_2404_10221_b200.solver import RsfdeSolver, RsfdeTeam
+    prob = I.config_c5(M=2, nn=shape)
+    x = _dev(I.seeded_vector(77, prob.n))
+    S = RsfdeSolver.from_problem(prob)
+    F = S.compact_source(_dev(prob.f_closed(prob.t_half(0))))
+    cfg = S.cfg(restart=prob.restart, tol=prob.tol)
+    outs = []
+    for unfused in (False, True):
+        if unfused:
+            monkeypatch.setenv("RSFDE_TEAM_UNFUSED", "1")
+        T = RsfdeTeam(prob, nranks=P)
+        k = _host(T.matvec(L.OP_K, x, m=1))
+        a = _host(T.matvec(L.OP_A, x, m=1))
+        pr = _host(T.precond(L.PHAT_INV, x))
+        u = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
+        r = T.solve_steps(u, F=F, F_static=True, cfg=cfg)
+        outs.append((k, a, pr, _host(u), r["iters"]))
+        del T
+    monkeypatch.delenv("RSFDE_TEAM_UNFUSED")
+    for name, v0, v1 in zip(("K", "A", "P_hat^-1", "march"), outs[0][:4], outs[1][:4]):
+        assert np.array_equal(v0, v1), (name, float(np.abs(v0 - v1).max() / np.abs(v1).max()))
+    assert outs[0][4] == outs[1][4]
