@@ -436,15 +436,16 @@ F_host_steps = None
 
 def sharded_roofline(prob, ws, iters, t_max):
     """Solve-level roofline of a slab-sharded run (per rank, algorithmic pass model of DESIGN.md section 8):
-    HBM bytes per GMRES iteration at Arnoldi index j = vec_r (14 + 3j + 7) for the K chain and CGS2
-    plus 12 vec_r for the three pack/unpack transposes; NVLink bytes = 3 vec_r (P-1)/P sent per rank."""
+    HBM bytes per GMRES iteration at Arnoldi index j = vec_r (14 + 2j + 6) for the K chain and DCGS2
+    plus 6 vec_r for the exchanges (fused: pack A->T of the two channels, unpack T->A of the result; the
+    x1 pass reads and writes the all-to-all blocks itself); NVLink bytes = 3 vec_r (P-1)/P per rank."""
     hbm, src = measured_peaks()
     vec_r = 8.0 * prob.N / ws
     nit = sum(iters)
     hbm_bytes = nvl_bytes = 0.0
     for k in iters:
         for j in range(k):
-            hbm_bytes += vec_r * (14 + 3 * j + 7 + 12)
+            hbm_bytes += vec_r * (14 + 2 * j + 6 + 6)
             nvl_bytes += 3 * vec_r * (ws - 1) / ws
     ach = hbm_bytes / t_max / 1e9
     nvl = nvl_bytes / t_max / 1e9
