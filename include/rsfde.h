@@ -25,7 +25,10 @@
  *  - Unless stated otherwise vector arguments are caller-owned DEVICE pointers.  The ctx
  *    owns its tables, Krylov basis and work buffers (padded private layout).
  *  - A ctx is used by one host thread at a time.  Calls are stream-ordered; only GMRES
- *    calls synchronise the stream (once per Arnoldi step, to read the convergence flag).
+ *    calls synchronise the stream to read the convergence flags: once per GMRES cycle of a CN
+ *    step when the cycle runs as a captured CUDA graph (the default of rsfde_solve_steps, see
+ *    rsfde_graph_replays), once per Arnoldi step otherwise (one step ahead: the kernels of step
+ *    j+1 are already queued when the flags of step j are read).
  *  - Restriction: every n_i + 1 must be a power of two with 2 <= n_i + 1 <= 2048 (FFT lengths
  *    L = 2(n_i+1) <= 4096 are built); otherwise RSFDE_E_DIM.  The paper's grids (N+1 = 2^k,
  *    P:532-633) and all five BASELINE configs (n = 255, 255^2, 2047^2, 255^3, 511^3) satisfy it.
