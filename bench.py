@@ -141,6 +141,15 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def l2_note(prob) -> str:
+    """What the timed region does about L2 (timing rule: flush or inputs larger than L2)."""
+    vec = 8.0 * prob.N
+    if vec > 126e6:
+        return f"no flush: every vector ({vec / 1e9:.2f} GB) is larger than the 126 MB L2"
+    return (f"no flush: a vector is {vec / 1e6:.3g} MB and the working set of a step is L2-resident by design "
+            "(SURVEY 8(d): latency/launch-bound config, not an HBM roofline line)")
+
+
 def build_problem(workload: str):
     from paper_2404_10221_b200 import inputs as I
     if workload == "C5":
@@ -223,10 +232,13 @@ def run_reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload)},
+           "step_definition": "one bounded sample = ONE GMRES iteration of the oracle on the full grid of the "
+                              "workload (not a whole CN step: a C5 CN step is 7-8 such iterations plus the "
+                              "right-hand side); ms_per_step is per sample",
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                             "sample": "per step: one GMRES iteration of the oracle (Tier L dense per-line "
                                       "operators: K v = P_alpha^-1 A~ v + MGS vs 4 basis vectors) on the "
-                                      "full C5 grid"},
+                                      f"full {args.workload} grid"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -368,10 +380,11 @@ def run_ours(args):
         d = prof[dom]
         achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
         # DRAM bytes per launch of this kernel class from the committed ncu --set full capture of the
-        # C5 K chain (profiles/r01_ncu_traffic.json, tools/ncu_traffic.py); null for other workloads
+        # C5 K chain (newest profiles/rNN_ncu_traffic.json, tools/ncu_traffic.py); null for other workloads
         traffic, traffic_src = None, None
-        tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-        if os.path.exists(tp) and args.workload == "C5":
+        cands = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_ncu_traffic.json"))
+        tp = os.path.join(ROOT, "profiles", cands[-1]) if cands else ""
+        if cands and args.workload == "C5":
             with open(tp) as f:
                 tj = json.load(f)
             if dom in tj:
@@ -396,6 +409,13 @@ def run_ours(args):
                             "frac": ach / fp64_peak,
                             "note": "secondary: algorithmic 5 L log2 L flops per pair-FFT vs nominal FP64 peak "
                                     "(64 FMA/clk/SM x 2 x SMs x SM clock)"}
+    # solve-level (SURVEY 8(d) fractions 2 and 3): the algorithmic pass-model bytes of every launch of
+    # the profiled K steps over the device time of the timed region
+    tot_bytes = sum(v["bytes"] for v in prof.values())
+    solve = {"algorithmic_bytes_per_step": tot_bytes / args.steps,
+             "achieved": tot_bytes / t_dev / 1e9, "peak": peak, "unit": "GB/s",
+             "frac": tot_bytes / t_dev / 1e9 / peak,
+             "scope": "all kernels of a CN step: pass-model bytes (DESIGN.md section 6) / device time"}
     tot_ms = sum(v["ms"] for v in prof.values()) or 1.0
     breakdown = {k: {"share": v["ms"] / tot_ms, "ms": v["ms"], "launches": v["launches"],
                      "GBps": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] > 0 and v["bytes"] > 0 else None}
@@ -404,8 +424,8 @@ def run_ours(args):
     if ws == 1 and not args.no_cpu_baseline:
         t, threads = oracle_iteration_sample(prob)
         cpu = {"value": N / t, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": "one GMRES iteration of the oracle on the full C5 grid (Tier L per-line dense "
-                         "operators: K v = P_alpha^-1 A~ v + MGS vs 4 basis vectors), timed once",
+               "sample": f"one GMRES iteration of the oracle on the full {args.workload} grid (Tier L per-line "
+                         "dense operators: K v = P_alpha^-1 A~ v + MGS vs 4 basis vectors), timed once",
                "seconds": t}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -416,10 +436,9 @@ def run_ours(args):
         "config": {"workload": WORKLOAD_TEXT.get(args.workload, args.workload), "n": list(prob.n),
                    "M": prob.M, "restart": prob.restart, "tol": prob.tol, "unknowns": N,
                    "parallelism": "replicas" if ws > 1 else "single GPU",
-                   "l2": "no flush: every vector (1.07 GB) is larger than the 126 MB L2",
-                   "iters_per_step": iters},
-        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernel_breakdown": breakdown,
-        "cpu_baseline": cpu, "clocks": clk, "setup_seconds": setup_s,
+                   "l2": l2_note(prob), "iters_per_step": iters},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roof, "solve_level": solve,
+        "kernel_breakdown": breakdown, "cpu_baseline": cpu, "clocks": clk, "setup_seconds": setup_s,
         "device_bytes": S.device_bytes(),
     }
     print(json.dumps(out), flush=True)
