@@ -140,6 +140,17 @@ __device__ __forceinline__ void fft_fwd_pre(double2 (&v)[E], int g, const double
   dft<E>(v);
   twiddle_col<E, false>(v, tw, g, E * G);
 }
+// the exchange alone (E == G: one row per thread), for callers that schedule the second DFT themselves
+template <int E, int G>
+__device__ __forceinline__ void fft_exchange(double2 (&v)[E], double2* buf, int g) {
+  static_assert(E == G, "fft_exchange: square split");
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < E; ++k1) buf[xidx<E, G>(k1, g)] = v[k1];
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < G; ++t) v[t] = buf[xidx<E, G>(g, t)];
+}
 template <int E, int G>
 __device__ __forceinline__ void fft_fwd_post(double2 (&v)[E], double2* buf, int g) {
   constexpr int R = E / G;

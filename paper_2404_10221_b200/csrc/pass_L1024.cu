@@ -12,7 +12,8 @@ RSFDE_INSTANTIATE_T(T1024)
 // of one block)
 static int tile_pairs(const PassParams& p) {
   if (p.flags & PASS_FLAG_NO_PIPE) return 0;
-  if (p.contiguous) return 4;
+  const char* ct8 = getenv("RSFDE_TILE_CT8");  // contiguous axis: 8-pair tiles (x3 oper pass 1.82 -> 1.62 ms same-box; RSFDE_TILE_CT8=0: 4-pair tiles)
+  if (p.contiguous) return (ct8 && !strcmp(ct8, "0")) ? 4 : 8;
   // 128-byte rows where rows are >= 1 MB apart (x1 of the C5 grid: every row piece is its own 2 MB
   // page and the TMA rate follows the row-piece count; measured 2 % faster K chain).
   // RSFDE_TILE128=1 forces them on every eligible strided pass (test coverage at small sizes).

@@ -159,6 +159,15 @@ struct rsfde_team {
   // (segmented contiguous axis, PassParams::seg_lg), so only pack A->T and unpack T->A remain
   bool fused = false;
   long long blk = 0;
+  // chunked exchanges (fused only): the slab's s planes are cut into nchunk sub-slabs of sc planes; the
+  // all-to-all blocks are laid out [peer][chunk][x2l][x3][x1l < sc], so a (peer, chunk) piece is contiguous
+  // and the x1 pass sees segments of sc planes.  Chunk c's exchange runs on the exchange stream xs while
+  // the passes of chunk c+1 (way there) or the unpack and inverse DSTs of chunk c-1 (way back) run on
+  // the caller's stream.
+  int nchunk = 1, sc = 0;
+  long long blkc = 0;
+  cudaStream_t xs = nullptr;
+  cudaEvent_t ev_s[8] = {}, ev_x[8] = {};
   std::vector<ShardBufs> sh;
   ncclComm_t comm = nullptr;
   void* h_flags = nullptr;
@@ -253,6 +262,21 @@ static PassParams paramsT(const rsfde_team* t, int l) {
   return local_params(t, t->sh[l].gT, kPhysT, 2, coff);
 }
 
+// sub-slab c (planes [c sc, (c+1) sc) of the local slab) of layout A: chunk geometry, global x1 offset
+static PassParams paramsA_c(const rsfde_team* t, int l, int axis, int c) {
+  if (t->nchunk == 1) return paramsA(t, l, axis);
+  Geom g = t->sh[l].gA;
+  g.n[0] = t->sc;
+  g.NP = (long long)t->sc * g.n[1] * g.P;
+  const int coff[3] = {t->sh[l].x1lo + c * t->sc, 0, 0};
+  return local_params(t, g, kPhysA, axis, coff);
+}
+// element offset of sub-slab c inside a layout-A vector
+static long long chunk_off(const rsfde_team* t, int l, int c) {
+  const Geom& g = t->sh[l].gA;
+  return (long long)c * t->sc * g.n[1] * g.P;
+}
+
 static ECoef ecoefA(const rsfde_team* t, int m) {
   ECoef e = rsfde_ecoef_at(t->tab, m);  // separable tables indexed by global coordinates
   return e;
@@ -260,23 +284,26 @@ static ECoef ecoefA(const rsfde_team* t, int m) {
 
 // all-to-all of the shards' send buffers 0..nv-1 into their recv buffers (one NCCL group for all nv
 // vectors: the two channels of the operator chain travel in one exchange)
-static rsfde_status team_alltoall(rsfde_team* t, cudaStream_t s, int nv = 1) {
-  const size_t bytes = (size_t)t->blk * sizeof(double);
+// (chunk < 0: whole blocks; chunk c >= 0: the (peer, c) pieces of blkc elements)
+static rsfde_status team_alltoall(rsfde_team* t, cudaStream_t s, int nv = 1, int chunk = -1) {
+  const long long cnt = chunk < 0 ? t->blk : t->blkc;
+  const long long coff = chunk < 0 ? 0 : (long long)chunk * t->blkc;
+  const size_t bytes = (size_t)cnt * sizeof(double);
   if (!t->comm) {
     for (int v = 0; v < nv; ++v)
       for (int dst = 0; dst < t->P; ++dst)
         for (int src = 0; src < t->P; ++src)
-          TCK(cudaMemcpyAsync(t->sh[dst].recv[v] + (long long)src * t->blk, t->sh[src].send[v] + (long long)dst * t->blk,
-                              bytes, cudaMemcpyDeviceToDevice, s),
+          TCK(cudaMemcpyAsync(t->sh[dst].recv[v] + (long long)src * t->blk + coff,
+                              t->sh[src].send[v] + (long long)dst * t->blk + coff, bytes, cudaMemcpyDeviceToDevice, s),
               "alltoall copy");
     return RSFDE_OK;
   }
   TNC(g_nccl.GroupStart(), "ncclGroupStart");
   for (int v = 0; v < nv; ++v)
     for (int peer = 0; peer < t->P; ++peer) {
-      TNC(g_nccl.Send(t->sh[0].send[v] + (long long)peer * t->blk, (size_t)t->blk, ncclDouble, peer, t->comm, s),
+      TNC(g_nccl.Send(t->sh[0].send[v] + (long long)peer * t->blk + coff, (size_t)cnt, ncclDouble, peer, t->comm, s),
           "ncclSend");
-      TNC(g_nccl.Recv(t->sh[0].recv[v] + (long long)peer * t->blk, (size_t)t->blk, ncclDouble, peer, t->comm, s),
+      TNC(g_nccl.Recv(t->sh[0].recv[v] + (long long)peer * t->blk + coff, (size_t)cnt, ncclDouble, peer, t->comm, s),
           "ncclRecv");
     }
   TNC(g_nccl.GroupEnd(), "ncclGroupEnd");
@@ -335,40 +362,86 @@ static rsfde_status transpose_TA(rsfde_team* t, double* const* srcT, double* con
   return RSFDE_OK;
 }
 
-// fused exchanges: pack layout-A vectors into send buffers 0..nv-1 (one group), exchange
-static rsfde_status pack_send_AT(rsfde_team* t, const std::vector<std::vector<const double*>>& srcA, cudaStream_t s) {
+// fused exchanges, way there: pack sub-slab c of layout-A vectors into the (peer, c) pieces of send
+// buffers 0..nv-1 and start their exchange (one group) -- on the exchange stream when chunked, so that it
+// runs under the passes of the next sub-slab
+static rsfde_status pack_send_AT(rsfde_team* t, const std::vector<std::vector<const double*>>& srcA, int c,
+                                 cudaStream_t s) {
   const int nv = (int)srcA.size();
   for (int v = 0; v < nv; ++v)
     for (int l = 0; l < t->nlocal; ++l) {
       const ShardBufs& b = t->sh[l];
       const int n2 = t->tab->n[1], n3 = t->tab->n[2];
-      dim3 grid((n3 + 31) / 32, (t->s + 31) / 32, t->P * t->s2);
-      TCKL((pack_AT_kernel<<<grid, dim3(32, 8), 0, s>>>(srcA[v][l], b.send[v], t->s, n2, n3, b.gA.P, t->s2, t->blk),
+      dim3 grid((n3 + 31) / 32, (t->sc + 31) / 32, t->P * t->s2);
+      TCKL((pack_AT_kernel<<<grid, dim3(32, 8), 0, s>>>(srcA[v][l] + chunk_off(t, l, c), b.send[v] + (long long)c * t->blkc,
+                                                         t->sc, n2, n3, b.gA.P, t->s2, t->blk),
             cudaGetLastError()),
            "pack A->T");
     }
-  return team_alltoall(t, s, nv);
+  if (t->nchunk == 1) return team_alltoall(t, s, nv);
+  TCK(cudaEventRecord(t->ev_s[c], s), "event");
+  TCK(cudaStreamWaitEvent(t->xs, t->ev_s[c], 0), "wait");
+  return team_alltoall(t, t->xs, nv, c);
 }
-// ... and after the x1 pass wrote its send blocks: exchange, unpack into layout A
-static rsfde_status exchange_unpack_TA(rsfde_team* t, double* const* dstA, cudaStream_t s) {
-  TTRY(team_alltoall(t, s, 1));
-  for (int l = 0; l < t->nlocal; ++l) {
-    const ShardBufs& b = t->sh[l];
-    const int n2 = t->tab->n[1], n3 = t->tab->n[2];
-    dim3 grid((t->s + 31) / 32, (n3 + 31) / 32, t->P * t->s2);
-    TCKL((unpack_TA_kernel<<<grid, dim3(32, 8), 0, s>>>(b.recv[0], dstA[l], t->s, n2, n3, b.gA.P, t->s2, t->blk, b.s_real),
-          cudaGetLastError()),
-         "unpack T->A");
+// ... the caller's stream waits for every piece before the x1 pass
+static rsfde_status join_exchange(rsfde_team* t, cudaStream_t s) {
+  if (t->nchunk == 1) return RSFDE_OK;
+  TCK(cudaEventRecord(t->ev_x[0], t->xs), "event");
+  TCK(cudaStreamWaitEvent(s, t->ev_x[0], 0), "wait");
+  return RSFDE_OK;
+}
+// way back, after the x1 pass wrote its send blocks: exchange piece by piece; as soon as piece c is
+// here, unpack sub-slab c into layout A and (dst = true) run its inverse DSTs along x2 and x3
+// (W0 -> W1 -> out) under the exchange of piece c+1
+static rsfde_status exchange_unpack_TA(rsfde_team* t, double* const* dstA, bool dst, double* const* out,
+                                       cudaStream_t s) {
+  const int nc = t->nchunk;
+  if (nc > 1) {
+    TCK(cudaEventRecord(t->ev_s[0], s), "event");
+    TCK(cudaStreamWaitEvent(t->xs, t->ev_s[0], 0), "wait");
+    for (int c = 0; c < nc; ++c) {
+      TTRY(team_alltoall(t, t->xs, 1, c));
+      TCK(cudaEventRecord(t->ev_x[c], t->xs), "event");
+    }
+  } else {
+    TTRY(team_alltoall(t, s, 1));
+  }
+  for (int c = 0; c < nc; ++c) {
+    if (nc > 1) TCK(cudaStreamWaitEvent(s, t->ev_x[c], 0), "wait");
+    for (int l = 0; l < t->nlocal; ++l) {
+      const ShardBufs& b = t->sh[l];
+      const int n2 = t->tab->n[1], n3 = t->tab->n[2];
+      const int sreal = std::max(0, std::min(t->sc, b.s_real - c * t->sc));
+      dim3 grid((t->sc + 31) / 32, (n3 + 31) / 32, t->P * t->s2);
+      TCKL((unpack_TA_kernel<<<grid, dim3(32, 8), 0, s>>>(b.recv[0] + (long long)c * t->blkc, dstA[l] + chunk_off(t, l, c),
+                                                           t->sc, n2, n3, b.gA.P, t->s2, t->blk, sreal),
+            cudaGetLastError()),
+           "unpack T->A");
+    }
+    if (!dst) continue;
+    for (int l = 0; l < t->nlocal; ++l) {
+      ShardBufs& b = t->sh[l];
+      const long long off = chunk_off(t, l, c);
+      PassParams p = paramsA_c(t, l, 1, c);
+      p.X = b.W[0] + off;
+      p.Y = b.W[1] + off;
+      TCKL(launch_dst_pass(p, false, s), "dst x2");
+      PassParams q = paramsA_c(t, l, 2, c);
+      q.X = b.W[1] + off;
+      q.Y = out[l] + off;
+      TCKL(launch_dst_pass(q, false, s), "dst x3");
+    }
   }
   return RSFDE_OK;
 }
-// x1-pass parameters on the receive blocks (segmented contiguous axis: segments of s planes)
+// x1-pass parameters on the receive blocks (segmented contiguous axis: segments of sc planes, one per
+// (peer, chunk) piece)
 static PassParams paramsT_seg(const rsfde_team* t, int l) {
   PassParams p = paramsT(t, l);
   int lg = 0;
-  while ((1 << lg) < t->s) ++lg;
+  while ((1 << lg) < t->sc) ++lg;
   p.seg_lg = lg;
-  p.seg_stride = t->blk;
+  p.seg_stride = t->blkc;
   return p;
 }
 
@@ -384,45 +457,55 @@ struct TChain {
 // sharded operator chain (see the file header); out[l] in layout A, must not alias the inputs
 static rsfde_status team_chain(rsfde_team* t, const TChain& a, double* const* out, cudaStream_t s) {
   const int nl = t->nlocal;
-  // pass along x3 (layout A, contiguous), first pass: X channel from the caller
-  for (int l = 0; l < nl; ++l) {
-    ShardBufs& b = t->sh[l];
-    PassParams p = paramsA(t, l, 2);
-    p.xmode = a.xmode;
-    p.X = a.xmode == X_INPUT ? a.Xin[l] : nullptr;
-    p.R = a.R[l];
-    p.rscale = a.rscale.empty() ? nullptr : a.rscale[l];
-    p.eta = a.etafac * t->tab->eta[2];
-    if (a.xmode == X_E_TIMES_R) p.e = ecoefA(t, a.m);
-    p.spec.kind = a.spec;
-    p.Y = b.W[0];
-    p.C = b.W[1];
-    TCKL(launch_oper_pass(p, a.spectral, false, s), "pass x3");
-  }
-  // pass along x2 (layout A, strided)
-  for (int l = 0; l < nl; ++l) {
-    ShardBufs& b = t->sh[l];
-    PassParams p = paramsA(t, l, 1);
-    p.xmode = X_INPUT;
-    p.X = b.W[0];
-    p.R = b.W[1];
-    p.eta = a.etafac * t->tab->eta[1];
-    p.spec.kind = a.spec;
-    p.Y = b.W[2];
-    p.C = b.W[3];
-    TCKL(launch_oper_pass(p, a.spectral, false, s), "pass x2");
-  }
   const bool addB = !a.spectral && !a.B.empty() && a.B[0];
+  // passes along x3 and x2 on sub-slab c (the whole slab when not chunked)
+  auto passes_x3_x2 = [&](int c, bool chunked) -> rsfde_status {
+    // pass along x3 (layout A, contiguous), first pass: X channel from the caller
+    for (int l = 0; l < nl; ++l) {
+      ShardBufs& b = t->sh[l];
+      const long long off = chunked ? chunk_off(t, l, c) : 0;
+      PassParams p = chunked ? paramsA_c(t, l, 2, c) : paramsA(t, l, 2);
+      p.xmode = a.xmode;
+      p.X = a.xmode == X_INPUT ? a.Xin[l] + off : nullptr;
+      p.R = a.R[l] + off;
+      p.rscale = a.rscale.empty() ? nullptr : a.rscale[l];
+      p.eta = a.etafac * t->tab->eta[2];
+      if (a.xmode == X_E_TIMES_R) p.e = ecoefA(t, a.m);
+      p.spec.kind = a.spec;
+      p.Y = b.W[0] + off;
+      p.C = b.W[1] + off;
+      TCKL(launch_oper_pass(p, a.spectral, false, s), "pass x3");
+    }
+    // pass along x2 (layout A, strided)
+    for (int l = 0; l < nl; ++l) {
+      ShardBufs& b = t->sh[l];
+      const long long off = chunked ? chunk_off(t, l, c) : 0;
+      PassParams p = chunked ? paramsA_c(t, l, 1, c) : paramsA(t, l, 1);
+      p.xmode = X_INPUT;
+      p.X = b.W[0] + off;
+      p.R = b.W[1] + off;
+      p.eta = a.etafac * t->tab->eta[1];
+      p.spec.kind = a.spec;
+      p.Y = b.W[2] + off;
+      p.C = b.W[3] + off;
+      TCKL(launch_oper_pass(p, a.spectral, false, s), "pass x2");
+    }
+    return RSFDE_OK;
+  };
   if (t->fused) {
-    // both channels (and B) in one exchange; the x1 pass reads the receive blocks and writes the send
-    // blocks of the way back
+    // both channels (and B) in one exchange per sub-slab; the x1 pass reads the receive blocks and
+    // writes the send blocks of the way back
     std::vector<std::vector<const double*>> src(addB ? 3 : 2, std::vector<const double*>(nl));
     for (int l = 0; l < nl; ++l) {
       src[0][l] = t->sh[l].W[2];
       src[1][l] = t->sh[l].W[3];
       if (addB) src[2][l] = a.B[l];
     }
-    TTRY(pack_send_AT(t, src, s));
+    for (int c = 0; c < t->nchunk; ++c) {
+      TTRY(passes_x3_x2(c, true));
+      TTRY(pack_send_AT(t, src, c, s));
+    }
+    TTRY(join_exchange(t, s));
     for (int l = 0; l < nl; ++l) {
       ShardBufs& b = t->sh[l];
       PassParams p = paramsT_seg(t, l);
@@ -439,8 +522,11 @@ static rsfde_status team_chain(rsfde_team* t, const TChain& a, double* const* ou
     }
     std::vector<double*> dstA(nl);
     for (int l = 0; l < nl; ++l) dstA[l] = a.spectral ? t->sh[l].W[0] : out[l];
-    TTRY(exchange_unpack_TA(t, dstA.data(), s));
-  } else {
+    // (spectral: the inverse DSTs along x2 and x3 run per sub-slab inside)
+    return exchange_unpack_TA(t, dstA.data(), a.spectral, out, s);
+  }
+  TTRY(passes_x3_x2(0, false));
+  {
   // transpose both channels (and B) to layout T
   std::vector<double*> srcA(nl), dstT(nl);
   for (int l = 0; l < nl; ++l) { srcA[l] = t->sh[l].W[2]; dstT[l] = t->sh[l].T[0]; }
@@ -492,22 +578,31 @@ static rsfde_status team_chain(rsfde_team* t, const TChain& a, double* const* ou
 // sharded S Lambda^{-1} S for the spectrum kind (in[l] -> out[l], layout A)
 static rsfde_status team_precond(rsfde_team* t, int kind, double* const* in, double* const* out, cudaStream_t s) {
   const int nl = t->nlocal;
-  for (int l = 0; l < nl; ++l) {
-    ShardBufs& b = t->sh[l];
-    PassParams p = paramsA(t, l, 2);
-    p.X = in[l];
-    p.Y = b.W[0];
-    TCKL(launch_dst_pass(p, false, s), "dst x3");
-    PassParams q = paramsA(t, l, 1);
-    q.X = b.W[0];
-    q.Y = b.W[1];
-    TCKL(launch_dst_pass(q, false, s), "dst x2");
-  }
+  // forward DSTs along x3 and x2 on sub-slab c (the whole slab when not chunked)
+  auto dsts_x3_x2 = [&](int c, bool chunked) -> rsfde_status {
+    for (int l = 0; l < nl; ++l) {
+      ShardBufs& b = t->sh[l];
+      const long long off = chunked ? chunk_off(t, l, c) : 0;
+      PassParams p = chunked ? paramsA_c(t, l, 2, c) : paramsA(t, l, 2);
+      p.X = in[l] + off;
+      p.Y = b.W[0] + off;
+      TCKL(launch_dst_pass(p, false, s), "dst x3");
+      PassParams q = chunked ? paramsA_c(t, l, 1, c) : paramsA(t, l, 1);
+      q.X = b.W[0] + off;
+      q.Y = b.W[1] + off;
+      TCKL(launch_dst_pass(q, false, s), "dst x2");
+    }
+    return RSFDE_OK;
+  };
   std::vector<double*> srcA(nl), dstT(nl), srcT(nl), dstA(nl);
   if (t->fused) {
     std::vector<std::vector<const double*>> src(1, std::vector<const double*>(nl));
     for (int l = 0; l < nl; ++l) src[0][l] = t->sh[l].W[1];
-    TTRY(pack_send_AT(t, src, s));
+    for (int c = 0; c < t->nchunk; ++c) {
+      TTRY(dsts_x3_x2(c, true));
+      TTRY(pack_send_AT(t, src, c, s));
+    }
+    TTRY(join_exchange(t, s));
     for (int l = 0; l < nl; ++l) {
       ShardBufs& b = t->sh[l];
       PassParams p = paramsT_seg(t, l);
@@ -517,8 +612,10 @@ static rsfde_status team_precond(rsfde_team* t, int kind, double* const* in, dou
       TCKL(launch_dst_pass(p, true, s), "dst x1 (scaled)");
     }
     for (int l = 0; l < nl; ++l) dstA[l] = t->sh[l].W[0];
-    TTRY(exchange_unpack_TA(t, dstA.data(), s));
-  } else {
+    return exchange_unpack_TA(t, dstA.data(), true, out, s);
+  }
+  TTRY(dsts_x3_x2(0, false));
+  {
   for (int l = 0; l < nl; ++l) { srcA[l] = t->sh[l].W[1]; dstT[l] = t->sh[l].T[0]; }
   TTRY(transpose_AT(t, srcA.data(), dstT.data(), s));
   for (int l = 0; l < nl; ++l) {
@@ -781,6 +878,11 @@ void rsfde_team_destroy(rsfde_team* t) {
   cudaDeviceSynchronize();
   for (void* p : t->allocs) cudaFree(p);
   if (t->h_flags) cudaFreeHost(t->h_flags);
+  for (int c = 0; c < 8; ++c) {
+    if (t->ev_s[c]) cudaEventDestroy(t->ev_s[c]);
+    if (t->ev_x[c]) cudaEventDestroy(t->ev_x[c]);
+  }
+  if (t->xs) cudaStreamDestroy(t->xs);
   if (t->comm) g_nccl.CommDestroy(t->comm);
   if (t->tab) rsfde_destroy(t->tab);
   delete t;
@@ -827,6 +929,19 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     const char* uf = getenv("RSFDE_TEAM_UNFUSED");
     t->fused = nranks >= 2 && t->s <= 256 && !(uf && *uf && strcmp(uf, "0"));
   }
+  // chunked exchanges: RSFDE_TEAM_CHUNKS (default 4), reduced until sub-slabs of sc >= 2 planes divide s and
+  // the x1 pass sees at most 256 segments (one TMA box dimension)
+  t->nchunk = 1;
+  if (t->fused) {
+    const char* ce = getenv("RSFDE_TEAM_CHUNKS");
+    int nc = ce ? atoi(ce) : 4;
+    if (nc < 1) nc = 1;
+    if (nc > 8) nc = 8;
+    while (nc > 1 && (t->s % nc || t->s / nc < 2 || (long long)nranks * nc > 256)) --nc;
+    t->nchunk = nc;
+  }
+  t->sc = t->s / t->nchunk;
+  t->blkc = t->blk / t->nchunk;
   t->sh.resize(nlocal);
   auto fail = [&](rsfde_status e) {
     g_team_error = t->err;
@@ -874,6 +989,13 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     b.st = reinterpret_cast<GmresState*>(stp);
   }
   if (cudaMallocHost(&t->h_flags, 64) != cudaSuccess) return fail(RSFDE_E_NOMEM);
+  if (t->nchunk > 1) {
+    if (cudaStreamCreateWithFlags(&t->xs, cudaStreamNonBlocking) != cudaSuccess) return fail(RSFDE_E_CUDA);
+    for (int c = 0; c < 8; ++c)
+      if (cudaEventCreateWithFlags(&t->ev_s[c], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&t->ev_x[c], cudaEventDisableTiming) != cudaSuccess)
+        return fail(RSFDE_E_CUDA);
+  }
   if (nccl_id) {
     if (!g_nccl.load()) {
       t->err = "libnccl.so.2 not found";

@@ -32,6 +32,9 @@ namespace rsfde {
 #ifndef RSFDE_TILE_COOP_STORES  // strided axes: stage outputs in shared memory, store whole tile rows cooperatively
 #define RSFDE_TILE_COOP_STORES 1   // (0: 16-byte pieces straight from registers -- measured 17 % slower at 511^3)
 #endif
+#ifndef RSFDE_TILE_PINGPONG  // CW = 8: the two compute warps of a sub-partition take turns on the FP64 pipe
+#define RSFDE_TILE_PINGPONG 0
+#endif
 #ifndef RSFDE_TILE_TRACE  // experiments only: per-tile clock64 stamps of warp 0 of every CTA
 #define RSFDE_TILE_TRACE 0
 #endif
@@ -112,6 +115,32 @@ template <int CW>
 __device__ __forceinline__ void named_arrive(int id) {
   asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "n"(32 * (CW + kStoreWarps)) : "memory");
 }
+
+// FP64 ping-pong (CW = 8, one CTA per SM): compute warps w and w + 4 share a scheduler / FP64 pipe.
+// Left alone they fall into lockstep (both in an FFT's register phase, then both in the shared-memory
+// plumbing: the pass time is the SUM of its FP64 and shared-memory times, profiles/r02_tile_experiments.txt).
+// A token per sub-partition (named barriers 4 + s for warps 0-3, 8 + s for warps 4-7, 64 threads each)
+// is held during the register DFT bursts, so one warp's burst runs against the other's exchange, stage
+// reads and stores.  Strict alternation: warp w + 4 primes the token of warp w at kernel start; every
+// warp runs the same number of bursts (all warps of a CTA process the same tiles).
+template <int CW>
+struct PingPong {
+  static constexpr bool on = RSFDE_TILE_PINGPONG && CW == 8;
+  int mine, other;
+  __device__ __forceinline__ PingPong(int warp) : mine(4 + (warp & 3) + 4 * (warp >> 2)), other(4 + (warp & 3) + 4 * (1 - (warp >> 2))) {
+    if (on && warp >= 4) asm volatile("bar.arrive %0, 64;\n" ::"r"(other) : "memory");
+  }
+  __device__ __forceinline__ void acquire() const {
+    if (on) asm volatile("bar.sync %0, 64;\n" ::"r"(mine) : "memory");
+  }
+  __device__ __forceinline__ void release() const {
+    if (on) asm volatile("bar.arrive %0, 64;\n" ::"r"(other) : "memory");
+  }
+  // warps 0-3 absorb the last (unmatched) release of their partner
+  __device__ __forceinline__ void finish(int warp) const {
+    if (on && warp < 4) asm volatile("bar.sync %0, 64;\n" ::"r"(mine) : "memory");
+  }
+};
 
 // element offset of the first pencil of tile t (strided: pencil 16t; contiguous: row 16t)
 template <int TP, int NH, bool CT>
@@ -337,6 +366,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   }
   const int g = lane % G, w = warp * PPW + lane / G;  // FFT-group thread index, pencil pair in the tile
   double2* buf = bufs + w * L;
+  const PingPong<CW> pp(warp);
   const double rs = p.rscale ? __ldg(p.rscale) : 1.0;
   // The DST scale hs is applied once, early: to the input of a DST pass, to y = H X + eta T R in an
   // operator pass and to Lambda^-1 before the last inverse DST -- never to the row-layout outputs.
@@ -415,12 +445,17 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         if constexpr (E == G) {
           // phase 1 (the convolution's inverse FFT) is conj(FFT(conj(.))): the input conj is folded
           // into the spectrum scaling of phase 0 and the output conj into the stencil of phase 1
+          pp.acquire();
           fft_fwd_pre<E, G>(v, g, p.tw);
+          pp.release();
           if (!CT && pend_free) {  // the register-only first half overlaps the store warps' copy
             named_sync<CW>(3);
             pend_free = false;
           }
-          fft_fwd_post<E, G>(v, buf, g);
+          fft_exchange<E, G>(v, buf, g);
+          pp.acquire();
+          dft<G>(v);
+          pp.release();
         } else {
           if (!CT && pend_free) {
             named_sync<CW>(3);
@@ -761,6 +796,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     }
     TTRACE(6)
   }
+  pp.finish(warp);
 #if RSFDE_TILE_TRACE
   // count launches (the last compute thread to finish bumps the counter once per launch)
   __shared__ int done_warps;

@@ -133,3 +133,37 @@ def test_fused_exchanges_equal_explicit_transposes(shape, P, monkeypatch):
     for name, v0, v1 in zip(("K", "A", "P_hat^-1", "march"), outs[0][:4], outs[1][:4]):
         assert np.array_equal(v0, v1), (name, float(np.abs(v0 - v1).max() / np.abs(v1).max()))
     assert outs[0][4] == outs[1][4]
+
+
+@pytest.mark.parametrize("shape,P,chunks", [((511, 15, 31), 2, 4), ((255, 31, 63), 4, 2), ((255, 15, 31), 8, 4),
+                                            ((63, 31, 15), 2, 8)])
+def test_chunked_exchanges_equal_whole_slab_exchanges(shape, P, chunks, monkeypatch):
+    # chunked exchanges (sub-slabs of the x1 slab; piece c travels on the exchange stream while the
+    # passes of sub-slab c+1 / the unpack and inverse DSTs of sub-slab c-1 run on the caller's stream)
+    # against whole-slab exchanges (RSFDE_TEAM_CHUNKS=1): the same arithmetic per pencil, so K, A,
+    # P_hat^-1 and a march agree bit for bit -- and the chunked march agrees with the oracle-checked
+    # single-GPU path
+    from paper_2404_10221_b200 import _lib as L
+    from paper_2404_10221_b200.solver import RsfdeSolver, RsfdeTeam
+    prob = I.config_c5(M=2, nn=shape)
+    x = _dev(I.seeded_vector(78, prob.n))
+    S = RsfdeSolver.from_problem(prob)
+    F = S.compact_source(_dev(prob.f_closed(prob.t_half(0))))
+    cfg = S.cfg(restart=prob.restart, tol=prob.tol)
+    outs = []
+    for nc in (chunks, 1):
+        monkeypatch.setenv("RSFDE_TEAM_CHUNKS", str(nc))
+        T = RsfdeTeam(prob, nranks=P)
+        k = _host(T.matvec(L.OP_K, x, m=1))
+        a = _host(T.matvec(L.OP_A, x, m=1))
+        pr = _host(T.precond(L.PHAT_INV, x))
+        u = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
+        r = T.solve_steps(u, F=F, F_static=True, cfg=cfg)
+        outs.append((k, a, pr, _host(u), r["iters"]))
+        del T
+    monkeypatch.delenv("RSFDE_TEAM_CHUNKS")
+    for name, v0, v1 in zip(("K", "A", "P_hat^-1", "march"), outs[0][:4], outs[1][:4]):
+        assert np.array_equal(v0, v1), (name, float(np.abs(v0 - v1).max() / np.abs(v1).max()))
+    assert outs[0][4] == outs[1][4]
+    ks = _host(S.matvec(L.OP_K, x, m=1))
+    assert np.abs(outs[0][0] - ks).max() / np.abs(ks).max() < 1e-12
