@@ -225,7 +225,12 @@ int rsfde_profile_read(rsfde_ctx *ctx, int cls, long long *launches, double *ms,
  *             device copies);
  *             vectors are the whole dense grid.  Used by the single-GPU parity tests.
  * Same conventions as above otherwise (device pointers, stream-ordered, A form only).  The
- * coefficient must be RSFDE_COEF_SEPARABLE (a dense grid e is not sliced per rank): RSFDE_E_CONFIG. */
+ * coefficient must be RSFDE_COEF_SEPARABLE (a dense grid e is not sliced per rank): RSFDE_E_CONFIG.
+ * Streams: with nranks >= 2 the exchanges run piece by piece (sub-slabs of the x_1 slab,
+ * RSFDE_TEAM_CHUNKS, default 4) on an internal exchange stream that is event-ordered with `stream`
+ * in both directions: every call is still complete in `stream` order when it returns / when work
+ * enqueued on `stream` after it runs.  All ranks must issue the same calls in the same order (one
+ * NCCL communicator). */
 typedef struct rsfde_team rsfde_team;
 rsfde_status rsfde_nccl_unique_id(void *out128);
 rsfde_status rsfde_team_setup(rsfde_team **out, const rsfde_problem *p, int nranks, int rank, int nlocal,
@@ -237,6 +242,15 @@ rsfde_status rsfde_team_slab(const rsfde_team *t, int local, int *x1_lo, int *x1
    sends to each peer per transposed vector, laid out [x2 local < s2][x3 < n3][x1 local < s].
    RSFDE_E_DIM unless nranks divides n1+1 and n2+1; RSFDE_E_CONFIG for bad rank / nranks (1..8). */
 rsfde_status rsfde_team_partition(const int n[3], int nranks, int rank, int out[6], long long *block_elems);
+/* Host-only piece bookkeeping of the chunked exchanges (no device needed): for nranks >= 2 the slab's
+   s = (n1+1)/nranks planes are cut into out[0] = nchunk sub-slabs of out[1] = sc = s/nchunk planes --
+   `requested` (<= 0: the RSFDE_TEAM_CHUNKS environment value, default 4) reduced until sc >= 2 divides s
+   and nranks*nchunk <= 256 -- and every all-to-all block is laid out [chunk][x2 local < s2][x3 < n3]
+   [x1 local < sc]: *piece_elems = s2*n3*sc doubles per (peer, chunk) piece, piece c of the block for
+   peer r at offset r*block + c*piece.  The x_1 pencil (x2l, x3) of the receiving rank is the sequence of
+   segments (r'', c), r'' = 0..nranks-1, c = 0..nchunk-1, of sc planes each.  nranks = 1: nchunk = 1.
+   Errors as rsfde_team_partition. */
+rsfde_status rsfde_team_chunking(const int n[3], int nranks, int requested, int out[2], long long *piece_elems);
 /* op: RSFDE_OP_K (P_hat^{-1} A) or RSFDE_OP_A */
 rsfde_status rsfde_team_matvec(rsfde_team *t, int op, int m, const double *x, double *y, void *stream);
 rsfde_status rsfde_team_precond_apply(rsfde_team *t, int kind, const double *x, double *y, void *stream);

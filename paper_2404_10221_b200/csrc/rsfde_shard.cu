@@ -933,12 +933,9 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
   // the x1 pass sees at most 256 segments (one TMA box dimension)
   t->nchunk = 1;
   if (t->fused) {
-    const char* ce = getenv("RSFDE_TEAM_CHUNKS");
-    int nc = ce ? atoi(ce) : 4;
-    if (nc < 1) nc = 1;
-    if (nc > 8) nc = 8;
-    while (nc > 1 && (t->s % nc || t->s / nc < 2 || (long long)nranks * nc > 256)) --nc;
-    t->nchunk = nc;
+    int ch[2];
+    long long piece = 0;
+    if (rsfde_team_chunking(p->n, nranks, 0, ch, &piece) == RSFDE_OK) t->nchunk = ch[0];
   }
   t->sc = t->s / t->nchunk;
   t->blkc = t->blk / t->nchunk;
@@ -1007,6 +1004,25 @@ rsfde_status rsfde_team_setup(rsfde_team** out, const rsfde_problem* p, int nran
     if (r != ncclSuccess) return fail(nfail(t, r, "ncclCommInitRank"));
   }
   *out = t;
+  return RSFDE_OK;
+}
+
+rsfde_status rsfde_team_chunking(const int n[3], int nranks, int requested, int out[2], long long* piece_elems) {
+  if (!n || !out || nranks < 1 || nranks > 8) return RSFDE_E_CONFIG;
+  if (n[0] < 1 || n[1] < 1 || n[2] < 1) return RSFDE_E_DIM;
+  if ((n[0] + 1) % nranks || (n[1] + 1) % nranks) return RSFDE_E_DIM;
+  const int s = (n[0] + 1) / nranks, s2 = (n[1] + 1) / nranks;
+  int nc = requested;
+  if (nc <= 0) {
+    const char* ce = getenv("RSFDE_TEAM_CHUNKS");
+    nc = ce ? atoi(ce) : 4;
+  }
+  if (nc < 1 || nranks == 1) nc = 1;
+  if (nc > 8) nc = 8;
+  while (nc > 1 && (s % nc || s / nc < 2 || (long long)nranks * nc > 256)) --nc;
+  out[0] = nc;
+  out[1] = s / nc;
+  if (piece_elems) *piece_elems = (long long)s2 * n[2] * (s / nc);
   return RSFDE_OK;
 }
 

@@ -303,6 +303,19 @@ def team_partition(n, nranks: int, rank: int):
             "block": blk.value}
 
 
+def team_chunking(n, nranks: int, requested: int = 0):
+    """rsfde_team_chunking (host only): sub-slabs per slab, planes per sub-slab and doubles per
+    (peer, chunk) piece of the chunked exchanges."""
+    lib = L.load()
+    nn = (C.c_int * 3)(*[int(v) for v in n])
+    out = (C.c_int * 2)()
+    piece = C.c_longlong()
+    st = lib.rsfde_team_chunking(nn, nranks, requested, out, C.byref(piece))
+    if st != L.OK:
+        raise L.RsfdeError(st, "rsfde_team_chunking")
+    return {"nchunk": out[0], "sc": out[1], "piece": piece.value}
+
+
 class RsfdeTeam:
     """Slab-sharded 3D solver (x_1 slabs over ``nranks`` ranks).
 
