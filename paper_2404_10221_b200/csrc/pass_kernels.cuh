@@ -348,6 +348,27 @@ __device__ __forceinline__ void odd_extend(double2 (&v)[T::E], double2* buf, int
   }
 }
 
+// The same odd extension through warp shuffles (groups of G <= 32 lanes, Lay2 layouts): the mirror
+// L - j of j = g + G m is (G - g) + G (E - 1 - m) for g > 0 -- lane G - g of the group, register
+// E - 1 - m -- and G (E - m) for g = 0 (the lane's own register E - m; j = N is the zero).  No pair
+// buffer, so a tile whose staged outputs are still being copied out by the store warps does not wait
+// here, and half the shared-memory traffic of the buffer version (64 SHFL vs 32 16-byte accesses).
+template <class T>
+__device__ __forceinline__ void odd_extend_shfl(double2 (&v)[T::E], int g) {
+  constexpr int E = T::E, G = T::G;
+  static_assert(G <= 32, "odd_extend_shfl: one FFT group per (part of a) warp");
+  const int src = (G - g) & (G - 1);
+#pragma unroll
+  for (int m = E / 2; m < E; ++m) {
+    const double2 a = v[E - 1 - m];
+    double2 t;
+    t.x = __shfl_sync(0xffffffffu, a.x, src, G);
+    t.y = __shfl_sync(0xffffffffu, a.y, src, G);
+    if (g == 0) t = (m == E / 2) ? make_double2(0.0, 0.0) : v[E - m];
+    v[m] = make_double2(-t.x, -t.y);
+  }
+}
+
 // ---------------------------------------------------------------------------------- the kernel
 // Each group of G threads processes one pencil pair; the grid covers all pairs.  (A persistent
 // grid -- with L2 prefetch, or with cp.async double buffering of the next pair -- was measured

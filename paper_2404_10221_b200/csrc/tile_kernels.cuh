@@ -423,12 +423,13 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
       if (lane == 0) mbar_arrive(&empty_bar);
       ++job;
     }
+    // (shuffle form: no pair-buffer write, so the previous tile's staged outputs, which the store warps
+    // may still be copying out, are waited for only at the exchange of the FFT below)
+    // Strided tiles only (same-box A/B at 511^3: inverse DST x2 557 -> 540 us, last pass 1915 -> 1896 us;
+    // the contiguous-axis passes were 4 % slower with shuffles and keep the buffer form).
     if (!OPER) {
-      if (!CT && pend_free) {  // the previous tile's staged outputs may still be read by the store warps
-        named_sync<CW>(3);
-        pend_free = false;
-      }
-      odd_extend<T>(v, buf, g);
+      if (CT) odd_extend<T>(v, buf, g);
+      else odd_extend_shfl<T>(v, g);
     }
 
     const int first = OPER ? 0 : 2;
@@ -643,7 +644,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         }
         }  // X_INPUT
         TTRACE(10)
-        odd_extend<T>(v, buf, g);
+        if (CT) odd_extend<T>(v, buf, g);
+        else odd_extend_shfl<T>(v, g);
       } else if (ph == 2 && LAST) {
         // S y (row layout, k = g + G r for r < E/2) into the pair buffer, then Lambda^{-1} in a rolled
         // loop over the same k (small code: the spectrum kinds are a runtime switch)
@@ -656,9 +658,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
         if constexpr (E == G) {
           if (fast && !e_tab) {
             // row register m holds k = g + G m, which is also column index j = g + G m of this thread:
-            // the scaled values stay in registers and only the mirror half of the odd extension of the
-            // second DST passes through the pair buffer
-            __syncwarp();
+            // the scaled values stay in registers and the mirror half of the odd extension of the
+            // second DST comes from the partner lanes by shuffle
 #pragma unroll
             for (int m = 0; m < E / 2; ++m) {
               const int k = g + G * m;
@@ -675,15 +676,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
                 wv.y = pc.vq ? v[m].x * (rcp_nr(lq * lh) * icHq) : 0.0;
               }
               v[m] = wv;
-              buf[k] = wv;
             }
-            __syncwarp();
-#pragma unroll
-            for (int m = E / 2; m < E; ++m) {
-              const int j = g + G * m;
-              const double2 tt = (j == N) ? make_double2(0.0, 0.0) : buf[L - j];
-              v[m] = make_double2(-tt.x, -tt.y);
-            }
+            odd_extend_shfl<T>(v, g);
             done = true;
           }
         }
