@@ -96,3 +96,27 @@ def test_oracle_is_not_imported_by_the_product_path():
     pat = re.compile(r"^\s*(from\s+oracle\b|import\s+oracle\b)", re.M)
     for f in pathlib.Path(ROOT, "paper_2404_10221_b200").rglob("*.py"):
         assert not pat.search(f.read_text()), f
+
+
+def test_team_chunking_host_bookkeeping(monkeypatch):
+    # rsfde_team_chunking (host only): pieces tile the all-to-all block, sub-slabs keep >= 2 planes,
+    # at most 256 segments per x1 pencil; one rank never chunks; bad arguments fail with the same
+    # codes as rsfde_team_partition
+    from paper_2404_10221_b200 import _lib as L
+    from paper_2404_10221_b200.solver import team_chunking, team_partition
+    monkeypatch.delenv("RSFDE_TEAM_CHUNKS", raising=False)
+    for n, P, req, expect in [((511, 511, 511), 8, 0, (4, 16)), ((511, 511, 511), 2, 0, (4, 64)),
+                              ((511, 511, 511), 4, 8, (8, 16)), ((255, 255, 255), 8, 4, (4, 8)),
+                              ((15, 7, 5), 8, 4, (1, 2)), ((7, 7, 7), 2, 4, (2, 2)), ((511, 511, 511), 1, 4, (1, 512))]:
+        ch = team_chunking(n, P, req)
+        part = team_partition(n, P, 0)
+        assert (ch["nchunk"], ch["sc"]) == expect, (n, P, req, ch)
+        assert ch["nchunk"] * ch["sc"] == part["s"] and ch["nchunk"] * ch["piece"] == part["block"]
+        assert P * ch["nchunk"] <= 256 and (ch["sc"] >= 2 or ch["nchunk"] == 1)
+    monkeypatch.setenv("RSFDE_TEAM_CHUNKS", "2")
+    assert team_chunking((511, 511, 511), 8)["nchunk"] == 2      # requested <= 0: the environment value
+    assert team_chunking((511, 511, 511), 8, 8)["nchunk"] == 8   # an explicit request wins
+    with pytest.raises(L.RsfdeError):
+        team_chunking((510, 511, 511), 8)                        # nranks must divide n1 + 1
+    with pytest.raises(L.RsfdeError):
+        team_chunking((511, 511, 511), 9)
