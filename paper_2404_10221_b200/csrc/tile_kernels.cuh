@@ -35,6 +35,9 @@ namespace rsfde {
 #ifndef RSFDE_TILE_PINGPONG  // CW = 8: the two compute warps of a sub-partition take turns on the FP64 pipe
 #define RSFDE_TILE_PINGPONG 0
 #endif
+#ifndef RSFDE_TILE_TABS_SMEM  // c^ and lambda^H of the operator passes in shared memory (L = 1024 path)
+#define RSFDE_TILE_TABS_SMEM 1
+#endif
 #ifndef RSFDE_TILE_TRACE  // experiments only: per-tile clock64 stamps of warp 0 of every CTA
 #define RSFDE_TILE_TRACE 0
 #endif
@@ -364,6 +367,19 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
     }
     compute_bar<CW>();
   }
+  // The axis tables c^ (even: c^_k = c^_{L-k}, so N + 1 values) and lambda^H of the operator passes in
+  // shared memory: every tile reads them right where they are used, and a global load there is an exposed
+  // L1/L2 latency on each warp's dependency chain.  Only where the 8 KB fit beside two resident CTAs
+  // (same-box A/B: x3 pass 1616 -> 1575 us, last pass 1902 -> 1862 us, C4 chain -3 %; the 4-pair L = 1024
+  // kernels would drop to a smaller L1 carve-out and ran 22 % slower, so they keep the global loads).
+  constexpr bool TABS = RSFDE_TILE_TABS_SMEM && OPER && (CW == 8 || L <= 512);
+  __shared__ double chat_s[TABS ? N + 1 : 1], lamH_s[(TABS && !LAST) ? N : 1];
+  if constexpr (TABS) {
+    for (int j = threadIdx.x; j <= N; j += kComputeThreads) chat_s[j] = __ldg(p.chat + j);
+    if (!LAST)
+      for (int j = threadIdx.x; j < kN; j += kComputeThreads) lamH_s[j] = __ldg(p.lamH + j);
+    compute_bar<CW>();
+  }
   const int g = lane % G, w = warp * PPW + lane / G;  // FFT-group thread index, pencil pair in the tile
   double2* buf = bufs + w * L;
   const PingPong<CW> pp(warp);
@@ -481,7 +497,7 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
             if (!T::lower(r)) continue;
             const int k = T::rowk(g, r);
             const double2 zm = (k >= 1) ? buf[L - k] : make_double2(0.0, 0.0);
-            const double f = (k >= 1) ? crs * __ldg(p.lamH + k - 1) : 0.0;
+            const double f = (k >= 1) ? crs * (TABS ? lamH_s[k - 1] : __ldg(p.lamH + k - 1)) : 0.0;
             cv[i++] = make_double2(-(v[r].y - zm.y) * f, (v[r].x - zm.x) * f);
           }
           if (CT && E == G) {
@@ -543,12 +559,16 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           // scaled conj spectrum: the inverse FFT of phase 1 runs as a forward FFT (see above)
 #pragma unroll
           for (int r = 0; r < E; ++r) {
-            const double ch = __ldg(p.chat + T::rowk(g, r));
+            const int kk = T::rowk(g, r);
+            const double ch = TABS ? chat_s[T::lower(r) ? kk : L - kk] : __ldg(p.chat + kk);
             v[r] = make_double2(v[r].x * ch, -v[r].y * ch);
           }
         } else {
 #pragma unroll
-          for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
+          for (int r = 0; r < E; ++r) {
+            const int kk = T::rowk(g, r);
+            v[r] = c_scale(v[r], TABS ? chat_s[T::lower(r) ? kk : L - kk] : __ldg(p.chat + kk));
+          }
         }
       } else if (OPER && ph == 1) {
         // X channel from the stage (job 1) into the pair buffer (x = X, or e o R), then
