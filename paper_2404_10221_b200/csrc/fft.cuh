@@ -124,6 +124,30 @@ __device__ __forceinline__ void twiddle_col(double2 (&v)[E], const double2* __re
   }
 }
 
+// The same with the exactly loaded powers W_L^{8 a g} (a = 0: W_L^g itself) taken from a small shared
+// table tws[a * G + g] filled once per CTA (they depend on g only): a global load here sits at the head
+// of the recurrence chain of every FFT of every tile.
+template <int E, int G, bool INV>
+__device__ __forceinline__ void twiddle_col_s(double2 (&v)[E], const double2* tws, int g) {
+  const double2 w1 = tws[g];
+  double2 w = w1;
+#pragma unroll
+  for (int k1 = 1; k1 < E; ++k1) {
+    if ((k1 & 7) == 0) w = tws[(k1 >> 3) * G + g];
+    else if (k1 > 1) w = c_mul(w, w1);
+    v[k1] = INV ? c_mulc(v[k1], w) : c_mul(v[k1], w);
+  }
+}
+// fill: tws[a * G + g] = W_L^{8 a g} (a >= 1), tws[g] = W_L^g
+template <int E, int G>
+__device__ __forceinline__ void twiddle_table_fill(double2* tws, const double2* __restrict__ tw, int tid, int nthreads) {
+  constexpr int L = E * G;
+  for (int i = tid; i < (E / 8) * G; i += nthreads) {
+    const int a = i / G, g = i % G;
+    tws[i] = __ldg(tw + (a == 0 ? g : ((8 * a * g) & (L - 1))));
+  }
+}
+
 // XOR swizzle of the exchange buffer (row k1, column t) -> conflict-free 16-byte accesses
 template <int E, int G>
 __device__ __forceinline__ int xidx(int k1, int t) {
@@ -139,6 +163,11 @@ template <int E, int G>
 __device__ __forceinline__ void fft_fwd_pre(double2 (&v)[E], int g, const double2* __restrict__ tw) {
   dft<E>(v);
   twiddle_col<E, false>(v, tw, g, E * G);
+}
+template <int E, int G>
+__device__ __forceinline__ void fft_fwd_pre_s(double2 (&v)[E], int g, const double2* tws) {
+  dft<E>(v);
+  twiddle_col_s<E, G, false>(v, tws, g);
 }
 // the exchange alone (E == G: one row per thread), for callers that schedule the second DFT themselves
 template <int E, int G>

@@ -372,6 +372,14 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
   // L1/L2 latency on each warp's dependency chain.  Only where the 8 KB fit beside two resident CTAs
   // (same-box A/B: x3 pass 1616 -> 1575 us, last pass 1902 -> 1862 us, C4 chain -3 %; the 4-pair L = 1024
   // kernels would drop to a smaller L1 carve-out and ran 22 % slower, so they keep the global loads).
+  // (E == G DST passes: the four exactly loaded twiddle powers per lane of the FFT's twiddle stage, 2 KB;
+  // same-box A/B: inverse DST x2 538 -> 523 us, DST x3 477 -> 471 us; no gain in the operator passes)
+  constexpr bool TWS = RSFDE_TILE_TABS_SMEM && E == G && !OPER;
+  __shared__ double2 tw_s[TWS ? (E / 8) * G : 1];
+  if constexpr (TWS) {
+    twiddle_table_fill<E, G>(tw_s, p.tw, threadIdx.x, kComputeThreads);
+    compute_bar<CW>();
+  }
   constexpr bool TABS = RSFDE_TILE_TABS_SMEM && OPER && (CW == 8 || L <= 512);
   __shared__ double chat_s[TABS ? N + 1 : 1], lamH_s[(TABS && !LAST) ? N : 1];
   if constexpr (TABS) {
@@ -463,7 +471,8 @@ __global__ void __launch_bounds__(TileCfg<TP * T::G / 32>::kTileThreads, TileCfg
           // phase 1 (the convolution's inverse FFT) is conj(FFT(conj(.))): the input conj is folded
           // into the spectrum scaling of phase 0 and the output conj into the stencil of phase 1
           pp.acquire();
-          fft_fwd_pre<E, G>(v, g, p.tw);
+          if constexpr (TWS) fft_fwd_pre_s<E, G>(v, g, tw_s);
+          else fft_fwd_pre<E, G>(v, g, p.tw);
           pp.release();
           if (!CT && pend_free) {  // the register-only first half overlaps the store warps' copy
             named_sync<CW>(3);
