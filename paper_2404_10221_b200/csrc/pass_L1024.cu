@@ -7,20 +7,21 @@ namespace rsfde {
 using T1024 = Lay2<32, 32>;
 RSFDE_INSTANTIATE_T(T1024)
 
-// tile width in pencil pairs: 8 = 128-byte rows (one CTA of 8 compute warps per SM), 4 = 64-byte rows
-// (two CTAs of 4 compute warps per SM), 0 = no tile pipeline (a strided tile must be adjacent pencils
-// of one block)
+// tile width in pencil pairs: 8 (one CTA of 8 compute warps per SM; 128-byte row pieces on a strided
+// axis, 16 rows on the contiguous axis) wherever the geometry allows it, else 4 = 64-byte row pieces (two
+// CTAs of 4 compute warps per SM), 0 = no tile pipeline (a strided tile must be adjacent pencils of one
+// block).  With the axis tables in shared memory (8-warp kernels only: tile_kernels.cuh) the 8-pair tiles
+// are the faster ones on every axis of the 511^3 grid (same-box A/B, last session of round 2: x2 operator
+// pass 1517 -> 1462 us, inverse DST x2 524 -> 493 us; on x1, whose rows are 2 MB apart, 128-byte pieces were
+// already needed for the TMA rate).  RSFDE_TILE128=0 / RSFDE_TILE_CT8=0 select the 4-pair tiles on the
+// strided / contiguous axes (tests and experiments).
 static int tile_pairs(const PassParams& p) {
   if (p.flags & PASS_FLAG_NO_PIPE) return 0;
-  const char* ct8 = getenv("RSFDE_TILE_CT8");  // contiguous axis: 8-pair tiles (x3 oper pass 1.82 -> 1.62 ms same-box; RSFDE_TILE_CT8=0: 4-pair tiles)
+  const char* ct8 = getenv("RSFDE_TILE_CT8");
   if (p.contiguous) return (ct8 && !strcmp(ct8, "0")) ? 4 : 8;
-  // 128-byte rows where rows are >= 1 MB apart (x1 of the C5 grid: every row piece is its own 2 MB
-  // page and the TMA rate follows the row-piece count; measured 2 % faster K chain).
-  // RSFDE_TILE128=1 forces them on every eligible strided pass (test coverage at small sizes).
   const char* f128 = getenv("RSFDE_TILE128");
-  const bool force128 = f128 && strcmp(f128, "0");
-  const bool force64 = f128 && !strcmp(f128, "0");  // (experiments: 64-byte tiles everywhere)
-  if (p.inner % 16 == 0 && !force64 && (force128 || p.stride * 8 >= (1ll << 20))) return 8;
+  const bool force64 = f128 && !strcmp(f128, "0");
+  if (p.inner % 16 == 0 && !force64) return 8;
   return p.inner % 8 == 0 ? 4 : 0;
 }
 

@@ -392,10 +392,15 @@ def test_onchip_1d_march_matches_oracle_and_generic_path(restart, monkeypatch):
     assert relerr(u_on, uo) < 1e-9
 
 
-@pytest.mark.parametrize("kind,shape", [("c5", (511, 15, 31)), ("c5", (15, 511, 31)), ("c5", (511, 511))])
-def test_tile128_matvec_and_precond_parity(kind, shape, monkeypatch, cache):
-    # 128-byte tiles (8 pairs per CTA) serve the 2 MB-stride axis of C5; force them at small sizes
-    monkeypatch.setenv("RSFDE_TILE128", "1")
+@pytest.mark.parametrize("wide", ["1", "0"])
+@pytest.mark.parametrize("kind,shape", [("c5", (511, 15, 31)), ("c5", (15, 511, 31)), ("c5", (511, 511)),
+                                        ("c5", (31, 15, 511))])
+def test_tile128_matvec_and_precond_parity(kind, shape, wide, monkeypatch, cache):
+    # both tile widths of the L = 1024 pipeline on every axis kind: 8 pairs per CTA (the default: 128-byte
+    # row pieces on strided axes, 16 rows on the contiguous axis) and 4 pairs per CTA (RSFDE_TILE128=0 /
+    # RSFDE_TILE_CT8=0; still the fallback when the inner extent is not a multiple of 16)
+    monkeypatch.setenv("RSFDE_TILE128", wide)
+    monkeypatch.setenv("RSFDE_TILE_CT8", wide)
     test_matvec_parity(cache, kind, shape, 0)
     test_precond_parity(cache, kind, shape)
 
