@@ -58,6 +58,10 @@ struct rsfde_ctx {
   double* d_lamH[3] = {nullptr, nullptr, nullptr};
   double* d_q[3] = {nullptr, nullptr, nullptr};
   double* d_tq[3] = {nullptr, nullptr, nullptr};
+  // row-layout copies (PassParams::chat_rl ...), axes with L = 4096 only
+  double* d_chat_rl[3] = {nullptr, nullptr, nullptr};
+  double* d_lamH_rl[3] = {nullptr, nullptr, nullptr};
+  double* d_tq_rl[3] = {nullptr, nullptr, nullptr};
   // coefficient e
   int ekind = RSFDE_COEF_SEPARABLE;
   std::vector<double> a_half, b_half;

@@ -81,7 +81,7 @@ struct Fft3 {
     for (int i = 0; i < E; ++i) v[i].y = -v[i].y;
   }
 
-  __device__ static __forceinline__ int rowk(int t, int r) {
+  __host__ __device__ static __forceinline__ int rowk(int t, int r) {
     const int s = r / F, e = r % F;
     return (t / F) + E * ((t % F) * CS + s) + E * E * e;
   }

@@ -121,6 +121,10 @@ struct PassParams {
   const double* chat;    // circulant spectrum / L, length L
   const double2* tw;     // W_L^k, length L
   const double* lamH;    // H eigenvalues of this axis (length n)
+  // row-layout copies for the L = 4096 three-stage form Lay3<16, 16> (null otherwise): entry r G + t holds
+  // chat[k], lamH[k - 1], tq[k - 1] at k = rowk(t, r) (0 where k = 0 or k > n), so that the lanes of a warp
+  // read consecutive addresses instead of one 128-byte line each
+  const double *chat_rl, *lamH_rl, *tq_rl;
   int flags;             // PASS_FLAG_*
   // global coordinates of this (possibly sharded / transposed) grid: axis i of the local array
   // starts at global index coff[i] of a physical axis with cext[i] interior points; pencils whose
@@ -143,6 +147,8 @@ __device__ __forceinline__ bool skip_launch(const int* skip) {
 enum { PASS_FLAG_NO_PIPE = 1 };
 
 // host-side launchers (pass_kernels.cu)
+// idx[r G + t] = rowk(t, r) of Lay3<16, 16> (4096 entries): the index map of the row-layout tables
+void row_layout_4096(int* idx);
 cudaError_t launch_oper_pass(const PassParams& p, bool spectral, bool last, cudaStream_t s);
 cudaError_t launch_dst_pass(const PassParams& p, bool last, cudaStream_t s);
 

@@ -12,6 +12,11 @@ using T4096h = Lay3<16, 16>;
 RSFDE_INSTANTIATE_T(T4096)
 RSFDE_INSTANTIATE_T(T4096h)
 
+void row_layout_4096(int* idx) {
+  for (int r = 0; r < T4096h::E; ++r)
+    for (int t = 0; t < T4096h::G; ++t) idx[r * T4096h::G + t] = T4096h::FT::rowk(t, r);
+}
+
 bool fft3_e32() {
   const char* v = getenv("RSFDE_FFT3_E");  // (read per call: tests toggle it)
   return v && !strcmp(v, "32");

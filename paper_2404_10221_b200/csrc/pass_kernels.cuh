@@ -210,10 +210,14 @@ __device__ __forceinline__ double2 e_pair(const PassParams& p, const PairCtx& pc
 }
 
 // Lambda of both pencils at last-axis spectral index k (1..n)
+__device__ __forceinline__ double2 spec_pair_v(const PassParams& p, const PencilConsts& kc, double lh, double tq);
 __device__ __forceinline__ double2 spec_pair(const PassParams& p, const PencilConsts& kc, int k) {
   const Spec& S = p.spec;
-  const double lh = __ldg(S.lamH[p.axis] + k - 1);
-  const double tq = __ldg(S.tq[p.axis] + k - 1);
+  return spec_pair_v(p, kc, __ldg(S.lamH[p.axis] + k - 1), __ldg(S.tq[p.axis] + k - 1));
+}
+// the same from the table values lambda^H_k and eta q_k / lambda^H_k of the pass axis
+__device__ __forceinline__ double2 spec_pair_v(const PassParams& p, const PencilConsts& kc, double lh, double tq) {
+  const Spec& S = p.spec;
   const double lPp = S.ebar + kc.cP_p + tq, lPq = S.ebar + kc.cP_q + tq;
   switch (S.kind) {
     case SPEC_PHAT: return make_double2(lPp * (kc.cH_p * lh), lPq * (kc.cH_q * lh));
@@ -310,6 +314,8 @@ struct Lay2 {
   __device__ static __forceinline__ void sync() { __syncwarp(); }
   __device__ static __forceinline__ int rowk(int g, int r) { return row_k<E, G>(g, r); }
   __host__ __device__ static constexpr bool lower(int r) { return (r % G) < G / 2; }
+  __device__ static __forceinline__ int sw(int k) { return k; }  // row-layout staging index (see Lay3)
+  static constexpr bool ROWTAB = false;
   __device__ static __forceinline__ void fft(double2 (&v)[E], double2* buf, int g, const double2* __restrict__ tw,
                                              bool inv) {
     fft_any<E, G>(v, buf, g, tw, inv);
@@ -321,10 +327,19 @@ struct Lay3 {
   using FT = Fft3<E_, F>;
   static constexpr int E = FT::E, G = FT::G, L = FT::L, N = FT::N, GROUPS = 1, THREADS = FT::G;
   // E = 32: 3 / 6 CTAs per SM (L = 4096 / 2048, as measured in round 1); E <= 16: 128 registers
-  static constexpr int MINB = E == 32 ? (F == 2 ? 6 : 3) : (65536 / 128) / THREADS;
+  // 256-thread form (L = 4096): 3 CTAs per SM at 85 registers (small spills) beat 2 at 128: C3 5.02 -> 4.86 ms
+  // per CN step same-box (profiles/r02_c3_experiments.txt)
+  static constexpr int MINB = E == 32 ? (F == 2 ? 6 : 3) : (THREADS == 256 ? 3 : (65536 / 128) / THREADS);
   __device__ static __forceinline__ void sync() { __syncthreads(); }
   __device__ static __forceinline__ int rowk(int t, int r) { return FT::rowk(t, r); }
   __host__ __device__ static constexpr bool lower(int r) { return FT::lower(r); }
+  // Row-layout staging index.  The 8 lanes of a quarter-warp hold k = k1 + (E CS) a + ... with the same
+  // k1 and consecutive a: unswizzled, their 16-byte values fall into one bank group (ncu: 32 wavefronts
+  // per request against 4 ideal).  XOR the bank-group bits with a's low bits; column-order readers
+  // (8 consecutive j) see a permutation inside their aligned group of 8.
+  static constexpr int SWSH = ilog2c(E * (E / F));
+  static constexpr bool ROWTAB = E == 16 && F == 16;  // PassParams::chat_rl / lamH_rl / tq_rl are in this layout
+  __device__ static __forceinline__ int sw(int k) { return F >= 8 ? (k ^ ((k >> SWSH) & 7)) : k; }
   __device__ static __forceinline__ void fft(double2 (&v)[E], double2* buf, int t, const double2* __restrict__ tw,
                                              bool inv) {
     if (inv) FT::inv(v, buf, t, tw);
@@ -387,6 +402,7 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
   double2* buf = smem + grp * L;
   const double rs = p.rscale ? __ldg(p.rscale) : 1.0;  // lazy basis normalisation of the input
   const double hs = 0.5 * p.dst_scale;
+  const bool rl = T::ROWTAB && p.chat_rl != nullptr;  // spectral tables read in row layout (coalesced)
   {
     const long long pair = (long long)blockIdx.x * GROUPS + grp;
     const bool active = pair < p.npairs;
@@ -423,21 +439,22 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
         if (SPECTRAL && !LAST) {
           T::sync();
 #pragma unroll
-          for (int r = 0; r < E; ++r) buf[T::rowk(g, r)] = v[r];
+          for (int r = 0; r < E; ++r) buf[T::sw(T::rowk(g, r))] = v[r];
           T::sync();
 #pragma unroll
           for (int r = 0; r < E; ++r) {
             if (!T::lower(r)) continue;  // k >= N (compile-time in row layout)
             const int k = T::rowk(g, r);
             if (k >= 1) {
-              const double2 zk = v[r], zm = buf[L - k];
-              const double f = hs * __ldg(p.lamH + k - 1);
+              const double2 zk = v[r], zm = buf[T::sw(L - k)];
+              const double f = hs * (rl ? __ldg(p.lamH_rl + r * G + g) : __ldg(p.lamH + k - 1));
               st_pair(p, p.C, pc, k, make_double2(-(zk.y - zm.y) * f, (zk.x - zm.x) * f));
             }
           }
         }
 #pragma unroll
-        for (int r = 0; r < E; ++r) v[r] = c_scale(v[r], __ldg(p.chat + T::rowk(g, r)));
+        for (int r = 0; r < E; ++r)
+          v[r] = c_scale(v[r], rl ? __ldg(p.chat_rl + r * G + g) : __ldg(p.chat + T::rowk(g, r)));
       } else if (ph == 1) {
         // conv inverse done: column layout, T R at j = g + G m (m < E/2).
         // X channel at j, neighbours through the shared buffer
@@ -530,20 +547,21 @@ __global__ void __launch_bounds__(T::THREADS, T::MINB) pass_kernel(const PassPar
             const int k = T::rowk(g, r);
             double2 w = make_double2(0.0, 0.0);
             if (k >= 1) {
-              const double2 lam = spec_pair(p, kc, k);
+              const double2 lam = rl ? spec_pair_v(p, kc, __ldg(p.lamH_rl + r * G + g), __ldg(p.tq_rl + r * G + g))
+                                     : spec_pair(p, kc, k);
               w.x = pc.vp ? (-v[r].y * hs) / lam.x : 0.0;
               w.y = pc.vq ? (v[r].x * hs) / lam.y : 0.0;
             }
-            buf[k] = w;
+            buf[T::sw(k)] = w;
           }
           T::sync();
 #pragma unroll
           for (int m = 0; m < E; ++m) {
             const int j = g + G * m;
             if (m < E / 2) {
-              v[m] = buf[j];
+              v[m] = buf[T::sw(j)];
             } else {
-              const double2 t = (j == N) ? make_double2(0.0, 0.0) : buf[L - j];
+              const double2 t = (j == N) ? make_double2(0.0, 0.0) : buf[T::sw(L - j)];
               v[m] = make_double2(-t.x, -t.y);
             }
           }

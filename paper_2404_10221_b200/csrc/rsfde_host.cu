@@ -177,6 +177,20 @@ static rsfde_status build_axis_tables(rsfde_ctx* c, int i) {
   std::vector<double> tq(n);
   for (int k = 0; k < n; ++k) tq[k] = c->eta[i] * c->q_tab[i][k] / c->lamH_tab[i][k];
   TRY(upload(c, &c->d_tq[i], tq.data(), n));
+  if (L == 4096) {
+    std::vector<int> idx(L);
+    row_layout_4096(idx.data());
+    std::vector<double> a(L), b(L), d(L);
+    for (int e = 0; e < L; ++e) {
+      const int k = idx[e];
+      a[e] = chatL[k];
+      b[e] = (k >= 1 && k <= n) ? c->lamH_tab[i][k - 1] : 0.0;
+      d[e] = (k >= 1 && k <= n) ? tq[k - 1] : 0.0;
+    }
+    TRY(upload(c, &c->d_chat_rl[i], a.data(), L));
+    TRY(upload(c, &c->d_lamH_rl[i], b.data(), L));
+    TRY(upload(c, &c->d_tq_rl[i], d.data(), L));
+  }
   return RSFDE_OK;
 }
 
@@ -212,6 +226,9 @@ PassParams rsfde_axis_params(const rsfde_ctx* c, int axis) {
   p.chat = c->d_chat[axis];
   p.tw = c->d_tw[axis];
   p.lamH = c->d_lamH[axis];
+  p.chat_rl = c->d_chat_rl[axis];
+  p.lamH_rl = c->d_lamH_rl[axis];
+  p.tq_rl = c->d_tq_rl[axis];
   for (int i = 0; i < 3; ++i) {
     p.coff[i] = 0;
     p.cext[i] = c->n[i];
