@@ -124,6 +124,22 @@ __device__ __forceinline__ void twiddle_col(double2 (&v)[E], const double2* __re
   }
 }
 
+// The same for E <= 16 with the seed W_L^{8 g} read from the second half of the table (tw[L + g] =
+// W_L^{8 g}): consecutive g read consecutive addresses instead of one 128-byte line per lane
+// (ncu, three-stage L = 4096 kernels: the seed loads were 20 % of the global L1 tag requests).
+template <int E, bool INV>
+__device__ __forceinline__ void twiddle_col_x(double2 (&v)[E], const double2* __restrict__ tw, int g, int L) {
+  static_assert(E <= 16, "twiddle_col_x: one seed (k1 = 8)");
+  const double2 w1 = __ldg(tw + g);
+  double2 w = w1;
+#pragma unroll
+  for (int k1 = 1; k1 < E; ++k1) {
+    if (k1 == 8) w = __ldg(tw + L + g);
+    else if (k1 > 1) w = c_mul(w, w1);
+    v[k1] = INV ? c_mulc(v[k1], w) : c_mul(v[k1], w);
+  }
+}
+
 // The same with the exactly loaded powers W_L^{8 a g} (a = 0: W_L^g itself) taken from a small shared
 // table tws[a * G + g] filled once per CTA (they depend on g only): a global load here sits at the head
 // of the recurrence chain of every FFT of every tile.

@@ -29,10 +29,16 @@ struct Fft3 {
     return row * E + (c ^ ((row + (c >> 3)) & 7));
   }
 
+  // twiddles W_L^{g k1}: E <= 16 forms read their seed from the table's second half (coalesced)
+  __device__ static __forceinline__ void twid(double2 (&v)[E], const double2* __restrict__ tw, int g) {
+    if constexpr (E <= 16) twiddle_col_x<E, false>(v, tw, g, L);
+    else twiddle_col<E, false>(v, tw, g, L);
+  }
+
   __device__ static __forceinline__ void fwd(double2 (&v)[E], double2* buf, int t, const double2* __restrict__ tw) {
     const int k1 = t / F, a = t % F;
     dft<E>(v);
-    twiddle_col<E, false>(v, tw, t, L);
+    twid(v, tw, t);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < E; ++q) buf[ia(q, t)] = v[q];
@@ -40,7 +46,7 @@ struct Fft3 {
 #pragma unroll
     for (int b = 0; b < E; ++b) v[b] = buf[ia(k1, a + F * b)];
     dft<E>(v);
-    twiddle_col<E, false>(v, tw, E * a, L);  // W_G^{a c} = W_L^{E a c}
+    twid(v, tw, E * a);  // W_G^{a c} = W_L^{E a c}
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < E; ++c) buf[ib(k1, a, c)] = v[c];
@@ -67,7 +73,7 @@ struct Fft3 {
     __syncthreads();
 #pragma unroll
     for (int c = 0; c < E; ++c) v[c] = buf[ib(k1, a, c)];
-    twiddle_col<E, false>(v, tw, E * a, L);
+    twid(v, tw, E * a);
     dft<E>(v);  // over c -> index b (t' = a + F b)
     __syncthreads();
 #pragma unroll
@@ -75,7 +81,7 @@ struct Fft3 {
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < E; ++q) v[q] = buf[ia(q, t)];
-    twiddle_col<E, false>(v, tw, t, L);
+    twid(v, tw, t);
     dft<E>(v);  // over k1 -> index m
 #pragma unroll
     for (int i = 0; i < E; ++i) v[i].y = -v[i].y;

@@ -119,7 +119,7 @@ struct PassParams {
   Spec spec;
   // per-axis tables (device)
   const double* chat;    // circulant spectrum / L, length L
-  const double2* tw;     // W_L^k, length L
+  const double2* tw;     // W_L^k, length L, followed by the seeds W_L^{8k}, length L
   const double* lamH;    // H eigenvalues of this axis (length n)
   // row-layout copies for the L = 4096 three-stage form Lay3<16, 16> (null otherwise): entry r G + t holds
   // chat[k], lamH[k - 1], tq[k - 1] at k = rowk(t, r) (0 where k = 0 or k > n), so that the lanes of a warp

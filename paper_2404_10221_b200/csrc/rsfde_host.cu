@@ -162,16 +162,18 @@ static rsfde_status build_axis_tables(rsfde_ctx* c, int i) {
     c->lamH_tab[i][k - 1] = (double)(1.0L - (long double)c->alpha[i] / 6.0L * sn * sn);
   }
   // twiddles W_L^k = exp(-2 pi i k / L)
-  std::vector<double2> tw(L);
+  // (second half: the seeds W_L^{8k} in the order of k, read by twiddle_col_x with consecutive lanes)
+  std::vector<double2> tw(2 * L);
   for (int k = 0; k < L; ++k) {
     const long double ang = 2.0L * pi * (long double)k / (long double)L;
     tw[k] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
   }
+  for (int k = 0; k < L; ++k) tw[L + k] = tw[(8 * k) & (L - 1)];
   // eta_i = kappa_i tau / (2 h_i^alpha_i), h_i = 1/(n_i+1)
   const long double h = 1.0L / (long double)N;
   c->eta[i] = (double)((long double)c->kappa[i] * (long double)c->tau / (2.0L * powl(h, (long double)c->alpha[i])));
   TRY(upload(c, &c->d_chat[i], chatL.data(), L));
-  TRY(upload(c, &c->d_tw[i], tw.data(), L));
+  TRY(upload(c, &c->d_tw[i], tw.data(), 2 * L));
   TRY(upload(c, &c->d_lamH[i], c->lamH_tab[i].data(), n));
   TRY(upload(c, &c->d_q[i], c->q_tab[i].data(), n));
   std::vector<double> tq(n);
