@@ -432,12 +432,14 @@ __global__ void __launch_bounds__(256, 2) dcgs_update_kernel(BasisPtrs b, int i0
 
 // apply the stored rotations 0..j-1 to the column col[0..j+1], then form rotation j; returns the
 // rotated column in R's column j and updates g from gsave[j] (g_j before the rotation)
-__device__ void dcgs_rotate_column(GmresState* st, double* col, int j) {
+// (csr / snr: the stored rotations 0..j-1, staged in shared memory by the caller -- a serial chain of
+// global loads on one thread was most of the finishing kernels' 8-15 us)
+__device__ void dcgs_rotate_column(GmresState* st, double* col, int j, const double* csr, const double* snr) {
   double* R = st->H;
   for (int i = 0; i < j; ++i) {
     const double a = col[i], b = col[i + 1];
-    col[i] = st->cs[i] * a + st->sn[i] * b;
-    col[i + 1] = -st->sn[i] * a + st->cs[i] * b;
+    col[i] = csr[i] * a + snr[i] * b;
+    col[i + 1] = -snr[i] * a + csr[i] * b;
   }
   const double a = col[j], b = col[j + 1];
   const double den = hypot(a, b);
@@ -455,6 +457,16 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
                                                             int nblk, int j, double* vscale, const int* skip) {
   if (skip_launch(skip)) return;
   __shared__ double red[2 * 52 + 2];
+  // rows 0..j of the raw Hessenberg columns 0..j-1, the basis scales and the stored rotations, staged by
+  // all threads: thread 0's serial algebra below then reads shared memory only
+  __shared__ double sH[kLdH * 51], svs[52], scs[52], ssn[52];
+  for (int e = threadIdx.x; e < j * kLdH; e += blockDim.x)
+    if (e % kLdH <= j) sH[e] = st->Hraw[e];
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    svs[i] = vscale[i];
+    scs[i] = st->cs[i];
+    ssn[i] = st->sn[i];
+  }
   const int NT = 2 * j + 2;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   for (int t = wp; t < NT; t += (int)(blockDim.x >> 5)) {
@@ -466,7 +478,7 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
   __syncthreads();
   if (threadIdx.x != 0) return;
   double* Hr = st->Hraw;
-  const double sj = vscale[j];
+  const double sj = svs[j];
   if (j == 0) {
     // q_0 = s_0 V_0 is exactly normalised (explicit norm of r_0): one CGS pass, nu = 1
     const double gam = red[1] * sj;
@@ -479,8 +491,8 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
   double a[52], c[52], t[52], qtw[52];
   double ss = 0.0, sc = 0.0;
   for (int i = 0; i < j; ++i) {
-    a[i] = red[i] * vscale[i] * sj;
-    c[i] = red[j + i] * vscale[i];
+    a[i] = red[i] * svs[i] * sj;
+    c[i] = red[j + i] * svs[i];
     ss += a[i] * a[i];
     sc += a[i] * c[i];
   }
@@ -489,15 +501,18 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
   const double nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
   st->nu = nu;
   // column j-1: K q_{j-1} = Q_{j-1} h + nu1 u  and  u = Q_{j-1} a + nu q_j
-  const double nu1 = Hr[j + (j - 1) * kLdH];
+  const double nu1 = sH[j + (j - 1) * kLdH];
   double col[53];
   for (int i = 0; i < j; ++i) {
-    Hr[i + (j - 1) * kLdH] += nu1 * a[i];
-    col[i] = Hr[i + (j - 1) * kLdH];
+    const double h = sH[i + (j - 1) * kLdH] + nu1 * a[i];
+    sH[i + (j - 1) * kLdH] = h;
+    Hr[i + (j - 1) * kLdH] = h;
+    col[i] = h;
   }
+  sH[j + (j - 1) * kLdH] = nu1 * nu;
   Hr[j + (j - 1) * kLdH] = nu1 * nu;
   col[j] = nu1 * nu;
-  dcgs_rotate_column(st, col, j - 1);
+  dcgs_rotate_column(st, col, j - 1, scs, ssn);
   if (nu == 0.0) {
     // u_j lies in span(Q_{j-1}): column j-1 was exact (lucky breakdown); the update pass becomes a
     // no-op on V_j and finish_b is skipped; the y solve uses the j corrected columns
@@ -512,7 +527,7 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
   // K q_j = (w - Q_j t)/nu with t = Hbar_{0..j, 0..j-1} a  (K Q_{j-1} = Q_j Hbar)
   for (int l = 0; l <= j; ++l) {
     double v = 0.0;
-    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) v += Hr[l + i * kLdH] * a[i];
+    for (int i = (l > 0 ? l - 1 : 0); i < j; ++i) v += sH[l + i * kLdH] * a[i];
     t[l] = v;
   }
   for (int i = 0; i < j; ++i) qtw[i] = c[i];
@@ -521,8 +536,8 @@ __global__ void __launch_bounds__(256) dcgs_finish_a_kernel(GmresState* st, cons
   // q_j = (s_j V_j - sum_i a_i s_i V_i)/nu;  nu u_{j+1} = w - (qtw_j/nu) u - sum_i (c_i - qtw_j a_i/nu) q_i
   const double ej = qtw[j] / nu;
   for (int i = 0; i < j; ++i) {
-    st->cq[i] = -a[i] * vscale[i] / nu;
-    st->cu[i] = -(c[i] - ej * a[i]) * vscale[i];
+    st->cq[i] = -a[i] * svs[i] / nu;
+    st->cu[i] = -(c[i] - ej * a[i]) * svs[i];
   }
   st->cq[j] = sj / nu;
   st->cu[j] = -ej * sj;
@@ -540,7 +555,14 @@ __global__ void __launch_bounds__(256) dcgs_finish_b_kernel(GmresState* st, cons
     }
     return;
   }
-  const double nrm2 = block_sum_partials(pnrm, nblk);
+  // column j of the raw Hessenberg matrix and the stored rotations, staged by all threads (see finish_a)
+  __shared__ double scol[53], scs[52], ssn[52];
+  for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+    scol[i] = st->Hraw[i + j * kLdH];
+    scs[i] = st->cs[i];
+    ssn[i] = st->sn[i];
+  }
+  const double nrm2 = block_sum_partials(pnrm, nblk);  // (its barriers also publish the staged values)
   if (threadIdx.x != 0) return;
   double* Hr = st->Hraw;
   const double un = sqrt(nrm2);
@@ -548,9 +570,10 @@ __global__ void __launch_bounds__(256) dcgs_finish_b_kernel(GmresState* st, cons
   Hr[(j + 1) + j * kLdH] = un / nu;  // ||u_{j+1}|| (u' = nu u_{j+1})
   vscale[j + 1] = un > 0.0 ? 1.0 / un : 0.0;
   double col[53];
-  for (int i = 0; i <= j + 1; ++i) col[i] = Hr[i + j * kLdH];
+  for (int i = 0; i <= j; ++i) col[i] = scol[i];
+  col[j + 1] = un / nu;
   st->gsave[j] = st->g[j];
-  dcgs_rotate_column(st, col, j);
+  dcgs_rotate_column(st, col, j, scs, ssn);
   st->relres = fabs(st->g[j + 1]) / st->beta0;
   st->converged = st->relres <= tol ? 1 : 0;
   st->breakdown = (un == 0.0) ? 1 : 0;
